@@ -1,0 +1,45 @@
+# Build everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> product library + synth + oracle
+#   make oracle     -> CPU oracle only (gcc)
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -shared -cudart static
+CC        ?= gcc
+CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra -shared
+
+PKG       := paper_1805_07339_b200
+CSRC      := $(PKG)/csrc
+LIB       := $(PKG)/libscn.so
+LIB_SRCS  := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
+LIB_HDRS  := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/scn.h
+
+SYNTH_HOST := scn_synth/libscn_synth_host.so
+SYNTH_CUDA := scn_synth/libscn_synth_cuda.so
+ORACLE     := oracle/libscn_oracle.so
+MICRO      := tools/micro/k0
+
+all: $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE)
+
+lib: $(LIB)
+oracle: $(ORACLE) $(SYNTH_HOST)
+micro: $(MICRO)
+
+$(LIB): $(LIB_SRCS) $(LIB_HDRS)
+	$(NVCC) $(NVFLAGS) -Iinclude -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+
+$(SYNTH_HOST): scn_synth/synth_host.c scn_synth/scn_synth.h
+	$(CC) $(CFLAGS) $< -o $@
+
+$(SYNTH_CUDA): scn_synth/synth_cuda.cu scn_synth/synth_host.c scn_synth/scn_synth.h
+	$(NVCC) $(NVFLAGS) scn_synth/synth_cuda.cu -o $@
+
+$(ORACLE): oracle/scn_oracle.c scn_synth/synth_host.c scn_synth/scn_synth.h
+	$(CC) $(CFLAGS) oracle/scn_oracle.c scn_synth/synth_host.c -o $@
+
+$(MICRO): tools/micro/k0.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+clean:
+	rm -f $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(MICRO)
+
+.PHONY: all lib oracle micro clean
