@@ -1,0 +1,197 @@
+/* scn.h — C ABI of libscn.so: the B200-native data-parallel hot path of
+ * Scanner (Poms et al., arXiv 1805.07339): sampled-frame HIST, [-1,0]
+ * histogram-difference shot scoring and 2x box downsample over video tables.
+ *
+ * Citations: P:L### = PAPER.md line (section named), S:L### = SPEC.md line.
+ * Readings Q# of silent/ambiguous passages: DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only; no torch types. Device pointers are CUDA device
+ *     addresses owned by the caller (PyTorch allocates them); the library never
+ *     allocates device memory and never frees caller memory.
+ *   - Host objects (scn_table, scn_seq) are created by scn_*_create /
+ *     scn_sample_* / scn_seq_concat and freed by the matching *_destroy.
+ *   - scn_run_* only ENQUEUE work on the given stream (cudaStream_t passed as
+ *     void*; NULL = legacy default stream); they never synchronise the device.
+ *     Results are valid once the stream has been synchronised. Buffers must
+ *     stay alive until then.
+ *   - Errors: every call returns a scn_status; nothing throws across the ABI.
+ *     scn_last_error() returns a thread-local message for the last non-OK
+ *     status. A CUDA launch/runtime failure returns SCN_ECUDA.
+ *   - Determinism: every output is an exact integer function of the input;
+ *     it does not depend on the shard boundaries, the launch configuration or
+ *     the number of GPUs.
+ */
+#ifndef SCN_H
+#define SCN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SCN_OK = 0,
+  SCN_EINVAL = 1,        /* malformed argument (see each call) */
+  SCN_ERANGE = 2,        /* index outside [0,N), absent sparse row, end > M */
+  SCN_ECUDA = 3,         /* CUDA launch / copy failure */
+  SCN_EUNSUPPORTED = 4   /* bins outside [1,256] */
+} scn_status;
+
+typedef enum { SCN_MEM_DEVICE = 0, SCN_MEM_HOST = 1 } scn_mem;
+
+typedef struct scn_table scn_table; /* opaque host-side table metadata */
+typedef struct scn_seq scn_seq;     /* opaque sampled sequence */
+typedef struct { int64_t start, end; } scn_block; /* half-open row block [start,end) */
+
+const char* scn_last_error(void);
+const char* scn_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Tables. "Scanner represents video collections ... as tables" with "one row
+ * per video frame" (§3). A table binds num_rows RGB8 frames,
+ * HWC layout (row-major pixels, 3 bytes R,G,B), width*height*3 = F bytes each.
+ *   dense mode : base != NULL, row r at base + r*frame_stride_bytes;
+ *                frame_stride_bytes >= F and a multiple of 16; base 16-aligned.
+ *   sparse mode: base == NULL, row_ptrs[r] = address of row r or 0 if the row
+ *                is not resident (only sampled rows need to be, "only a
+ *                sparse set of intermediate sequence elements must be
+ *                computed"). Non-zero pointers must be 16-aligned. row_ptrs is
+ *                copied.
+ *   Every resident row must be readable for ceil16(F) bytes (the TMA bulk
+ *   copies move whole 16-byte granules).
+ *   where = SCN_MEM_DEVICE: rows are in HBM (scn_run_*).
+ *   where = SCN_MEM_HOST:   rows are in (preferably pinned) host memory
+ *                           (scn_run_pipeline_host only).
+ * Errors: EINVAL if num_rows < 0, width/height < 1, channels != 3,
+ *   width*height > 715827882 (the u32 shot-diff bound 6*W*H, reading Q13),
+ *   a bad stride or misaligned pointer, or both/neither of base/row_ptrs.
+ * ------------------------------------------------------------------------- */
+scn_status scn_table_create(int64_t num_rows, int32_t width, int32_t height, int32_t channels, int32_t where,
+                            const void* base, int64_t frame_stride_bytes, const uint64_t* row_ptrs,
+                            scn_table** out);
+void scn_table_destroy(scn_table* t);
+int64_t scn_table_rows(const scn_table* t);
+
+/* ---------------------------------------------------------------------------
+ * Sampling (§3.2 "Sampling operations ... can be defined by strides,
+ * ranges, or index lists"). The result is a sequence of M positions [0,M)
+ * (P:L201-202), position j bound to one table row. The frame address of each
+ * position is resolved at creation, so the table may be destroyed afterwards.
+ *   stride : rows {0, s, 2s, ...} < N (reading Q8); EINVAL if s < 1.
+ *   range  : for each block [a,b) in order, rows a, a+step, ... < b (reading
+ *            Q9); blocks sorted and disjoint (EINVAL), 0 <= a <= b <= N
+ *            (ERANGE), step >= 1 (EINVAL).
+ *   gather : the given rows, strictly increasing (EINVAL), in [0,N) (ERANGE)
+ *            (reading Q10).
+ * In sparse mode a sampled row may be absent (pointer 0); any scn_run_* that
+ * reads an absent position returns ERANGE (residency is checked per run, i.e.
+ * per work packet, "dependency analysis incrementally (at work packet
+ * granularity)"), so each rank only materialises its own shard.
+ * ------------------------------------------------------------------------- */
+scn_status scn_sample_stride(const scn_table* t, int64_t stride, scn_seq** out);
+scn_status scn_sample_range(const scn_table* t, const scn_block* blocks, int64_t n_blocks, int64_t step,
+                            scn_seq** out);
+scn_status scn_sample_gather(const scn_table* t, const int64_t* rows, int64_t n, scn_seq** out);
+
+/* Concatenate per-table sequences into one job sequence (one job
+ * per video, all scheduled together). Each part is its own slice: the stencil
+ * never crosses parts (reading Q6). Parts must share width, height and
+ * memory location (EINVAL). Parts are copied; they may be destroyed after. */
+scn_status scn_seq_concat(const scn_seq* const* parts, int32_t n, scn_seq** out);
+
+int64_t scn_seq_length(const scn_seq* s);
+/* Introspection: part index and table row of every position (host arrays of
+ * length M; either may be NULL), and segment-start flags (1 at the first
+ * position of each part). */
+scn_status scn_seq_rows(const scn_seq* s, int32_t* part, int64_t* row);
+scn_status scn_seq_seg_starts(const scn_seq* s, uint8_t* flags);
+
+/* Contiguous shard of positions for rank r of G (reading
+ * Q17): [floor(r*M/G), floor((r+1)*M/G)). EINVAL if G < 1 or r outside [0,G). */
+scn_status scn_shard_range(int64_t m, int32_t world, int32_t rank, int64_t* begin, int64_t* end);
+/* 1 if the [-1,0] stencil at position `begin` needs the halo position
+ * begin-1 (begin > 0 and begin is not a segment start), else 0 (P:L214 warmup
+ * as redundant work; P:L255 the warmup is "treated like a stencil"). */
+int32_t scn_seq_needs_halo(const scn_seq* s, int64_t begin);
+
+/* Device metadata for scn_run_*: per-position frame address (u64) and
+ * segment-start flag (u8). scn_seq_device_bytes() bytes of caller-owned
+ * device memory; the upload is enqueued on `stream` and the workspace must
+ * stay alive while runs use it. Host-location sequences need no upload. */
+size_t scn_seq_device_bytes(const scn_seq* s);
+scn_status scn_seq_upload(scn_seq* s, void* d_workspace, size_t bytes, void* stream);
+void scn_seq_destroy(scn_seq* s);
+
+/* ---------------------------------------------------------------------------
+ * Runs over positions [begin, end) of an uploaded device-location sequence
+ * (one rank's shard). Outputs hold rows for [begin,end) only, row j-begin for
+ * position j. EINVAL if begin > end, not uploaded, or a host-location seq;
+ * ERANGE if end > M; EUNSUPPORTED if bins outside [1,256].
+ * ------------------------------------------------------------------------- */
+
+/* HIST (§5.1.2 "Compute and store the pixel color histogram for all
+ * frames"): d_hist[j][c][b] (u32, [end-begin][3][bins]) = number of pixels of
+ * frame j whose channel c value v has floor(v*bins/256) == b (readings
+ * Q1-Q3). d_hist is zeroed by the call. */
+scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t* d_hist,
+                             void* stream);
+
+/* Shot-diff ("detect shot boundaries (via histogram differences)") as
+ * a [-1,0] stencil over the sampled sequence (fig:sampling-f; reading
+ * Q7): d_diff[j] (u32) = sum_c sum_b |H[j][c][b] - H[j-1][c][b]|, and 0 at the
+ * first position of a part (reading Q6). d_hist holds rows [begin,end) from
+ * scn_run_histogram with the same bins. If scn_seq_needs_halo(s, begin), the
+ * histogram of position begin-1 is recomputed into d_scratch (>= 3*bins u32)
+ * rather than communicated (the shard's halo). */
+scn_status scn_run_shotdiff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, const uint32_t* d_hist,
+                            uint32_t* d_diff, uint32_t* d_scratch, void* stream);
+
+/* HIST and shot-diff in one pass: the halo frame (if any) rides in the same
+ * histogram launch as the shard's frames. Same outputs as the two calls. */
+scn_status scn_run_hist_shotdiff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t* d_hist,
+                                 uint32_t* d_diff, uint32_t* d_scratch, void* stream);
+
+/* 2x integer box downsample ("downsamples the resulting frames
+ * (Resize)"): d_out[j] (u8, [end-begin][H/2][W/2][3]) with
+ * O[y][x][c] = (P(2y,2x)+P(2y,2x+1)+P(2y+1,2x)+P(2y+1,2x+1)+2) >> 2; a
+ * trailing odd row/column is dropped (reading Q11). */
+scn_status scn_run_downsample(const scn_seq* s, int64_t begin, int64_t end, uint8_t* d_out, void* stream);
+
+/* HIST + downsample of the same sampled frames in one read of each frame
+ * (reading Q12: siblings over the sampled full-resolution frame). Outputs
+ * identical to scn_run_histogram + scn_run_downsample. */
+scn_status scn_run_hist_downsample(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t* d_hist,
+                                   uint8_t* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * End-to-end run over a HOST-location sequence: frames are streamed
+ * host->device in chunks through the caller's staging buffer, double-buffered
+ * so the copy of chunk k+1 overlaps the kernels on chunk k (P:L248
+ * "pipelining of CPU-GPU data transfers ... with graph operation execution").
+ *   ops: bit 0 = HIST, bit 1 = shot-diff (needs HIST), bit 2 = downsample.
+ *   d_staging: caller device memory, staging_bytes >= 2 * (ceil16(F) + 16)
+ *              (two chunks of at least one frame each; more = larger chunks).
+ *   d_scratch: >= 3*bins u32 when shot-diff needs a halo.
+ *   copy_stream: second stream for the H2D copies (may equal stream).
+ * Outputs as the device-location calls. Only enqueues work (host frames
+ * must stay valid until `stream` completes).
+ * ------------------------------------------------------------------------- */
+#define SCN_OP_HIST 1u
+#define SCN_OP_SHOTDIFF 2u
+#define SCN_OP_DOWNSAMPLE 4u
+scn_status scn_run_pipeline_host(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t ops,
+                                 uint32_t* d_hist, uint32_t* d_diff, uint8_t* d_out, uint32_t* d_scratch,
+                                 void* d_staging, size_t staging_bytes, void* stream, void* copy_stream);
+
+/* Launch statistics for the last scn_run_* call on this thread: number of
+ * kernels launched and the histogram kernel variant used (for bench.py's
+ * gpu_launches count). */
+int32_t scn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCN_H */

@@ -1,0 +1,597 @@
+// kernels.cu — sm_100a kernels of the Scanner HIST / shot-diff / downsample
+// hot path (arXiv 1805.07339 P:L331 HIST, P:L455 shot boundaries via
+// histogram differences over a [-1,0] stencil P:L210, P:L183/P:L335 resize).
+//
+// K1+K2 hist_pair_kernel<LOGB>  (bins = 2^LOGB <= 16; the configs' B = 16)
+//   Persistent, one CTA per SM (227 KB smem). Warp 16 is a TMA producer: one
+//   elected lane streams 30,720-byte tiles of the sampled frames with 1-D bulk
+//   copies (cp.async.bulk -> UBLKCP) into a 4-stage shared-memory ring guarded
+//   by full/empty mbarriers. Warps 0-15 consume: each thread takes 48-byte
+//   units (16 pixels, 3 x LDS.128, channel of byte j = j mod 3) and counts
+//   PAIRS of same-channel neighbours: key = (bin(a) << LOGB) | bin(b) into a
+//   lane-private table tab[c][key][lane] (bank == lane: conflict-free for any
+//   content) with one red.shared.add per pair, i.e. 0.5 shared atomics per
+//   byte. K0 measured 14.5 conflict-free lane-atomics/clk/SM on B200, so a
+//   per-byte scheme caps at ~62% of the HBM copy peak; pairs lift the cap
+//   above the HBM read rate. On a frame change the CTA's consumer warps
+//   marginalise the table (sum over lanes and the partner bin) into 3*B
+//   counters and merge them with one red.global.add each ("one global merge
+//   per block" per frame segment).
+// K2g hist_single_kernel: any bins in [1,256], one atomic per byte, same ring.
+// K2f hist_ds_kernel<LOGB>: K1+K2 with the 2x box downsample fused into the
+//   consumer (a thread takes the two vertically adjacent 48-byte units of a
+//   row pair, histograms both and emits 8 output pixels), so each sampled
+//   frame is read from HBM once (reading Q12).
+// K3 shotdiff_kernel: one warp per position, L1 over 3*B counters with
+//   __reduce_add_sync.
+// K4 downsample_kernel: LDG.128-vectorised 2x box downsample.
+//
+// Why not the north_star's per-warp bins + __match_any_sync aggregation: on
+// this B200 MATCH.ANY issues at 0.035 warp-instr/clk/SM (profiles/
+// r01_k0_micro.json), i.e. ~1.1 bytes/clk/SM if applied per byte, ~5% of the
+// HBM roofline. DESIGN.md §5 records the deviation and the evidence.
+#include "kernels.h"
+#include "ptx.cuh"
+
+#include <cstdio>
+#include <utility>
+
+namespace scn {
+
+constexpr int kConsWarps = 16;
+constexpr int kConsThreads = kConsWarps * 32;
+constexpr int kThreads = kConsThreads + 32;
+constexpr uint32_t kTile = 30720;  // 640 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA)
+constexpr int kMaxStages = 8;
+constexpr uint32_t kCtrlBytes = 1024;
+constexpr uint32_t kBarId = 1;     // named barrier among consumer warps
+
+struct HistParams {
+  FrameSrc src;
+  int64_t n_items;
+  int32_t n_halo;
+  uint32_t* out;
+  uint32_t* halo_out;
+  uint8_t* ds_out;
+  int64_t F;
+  int32_t width, height, bins;
+  uint32_t tile;          // bytes per full tile
+  int32_t rows_per_tile;  // fused kernel: rows per tile (even); 0 otherwise
+  int32_t tpf;            // tiles per frame
+  int64_t total_tiles;
+  uint32_t smem_bytes;
+  uint32_t table_bytes;
+  uint32_t table_align;
+};
+
+__device__ __forceinline__ uint64_t frame_addr(const FrameSrc& s, int64_t i) {
+  return s.ptrs ? s.ptrs[i] : s.base + (uint64_t)i * s.stride;
+}
+
+struct Layout {
+  uint32_t ctrl;   // [full bars][empty bars][hsum]
+  uint32_t table;
+  uint32_t gap_base, after_base, stride;
+  int n_gap, stages;
+  __device__ __forceinline__ uint32_t slot(int s) const {
+    return s < n_gap ? gap_base + (uint32_t)s * stride : after_base + (uint32_t)(s - n_gap) * stride;
+  }
+};
+
+// Shared-memory layout: control block, then the lane-private table aligned to
+// table_align (so bin fields can be OR-ed into its address), tile slots in the
+// gap before the table and after it.
+__device__ __forceinline__ Layout make_layout(uint32_t base, uint32_t smem_bytes, uint32_t tile, uint32_t tb_bytes,
+                                              uint32_t tb_align) {
+  Layout L;
+  L.ctrl = base;
+  const uint32_t end = base + smem_bytes;
+  const uint32_t t = (base + kCtrlBytes + tb_align - 1) & ~(tb_align - 1);
+  L.table = t;
+  L.stride = (tile + 127) & ~127u;
+  L.gap_base = (base + kCtrlBytes + 127) & ~127u;
+  L.n_gap = t >= L.gap_base + tile ? (int)((t - L.gap_base - tile) / L.stride) + 1 : 0;
+  L.after_base = (t + tb_bytes + 127) & ~127u;
+  const int n_after = end >= L.after_base + tile ? (int)((end - L.after_base - tile) / L.stride) + 1 : 0;
+  L.stages = L.n_gap + n_after;
+  if (L.stages > kMaxStages) L.stages = kMaxStages;
+  return L;
+}
+
+template <int OFF>
+__device__ __forceinline__ void red_shared_add_off(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
+}
+
+// Bits [8-LOGB, 8) of byte J of the unit (the bin of that byte for B = 2^LOGB),
+// moved to bit DST of the result.
+template <int J, int DST, int LOGB>
+__device__ __forceinline__ uint32_t bin_field(const uint32_t* w) {
+  constexpr int src = 8 * (J & 3) + 8 - LOGB;
+  const uint32_t x = w[J >> 2];
+  uint32_t y;
+  if constexpr (src >= DST) y = x >> (src - DST);
+  else y = x << (DST - src);
+  return y & (((1u << LOGB) - 1u) << DST);
+}
+
+// Byte J of the unit shifted so its top LOGB bits (its bin) land at bit DST (unmasked).
+template <int J, int DST, int LOGB>
+__device__ __forceinline__ uint32_t bin_shift(const uint32_t* w) {
+  constexpr int src = 8 * (J & 3) + 8 - LOGB;
+  const uint32_t x = w[J >> 2];
+  if constexpr (src >= DST) return x >> (src - DST);
+  else return x << (DST - src);
+}
+// (a & b) | c in one LOP3
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
+  return d;
+}
+
+// Count the 24 same-channel pixel pairs of one 48-byte unit (16 pixels).
+// lane4 = table base | lane << 2. Pair (2q, 2q+1) of channel c: bytes 6q+c, 6q+3+c.
+template <int LOGB, int P>
+__device__ __forceinline__ void pair_unit_step(const uint32_t* w, uint32_t lane4) {
+  constexpr int q = P / 3, c = P % 3;
+  constexpr int JA = 6 * q + c, JB = 6 * q + 3 + c;
+  constexpr int B = 1 << LOGB;
+  // addr = (yA & maskA) | ((yB & maskB) | lane4): two LOP3s (forced; the compiler emits three)
+  const uint32_t lo = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<JB, 7, LOGB>(w), lane4);
+  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << (7 + LOGB)>(bin_shift<JA, 7 + LOGB, LOGB>(w), lo);
+  red_shared_add_off<c * B * B * 128>(addr);
+}
+template <int LOGB, int... P>
+__device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
+  (pair_unit_step<LOGB, P>(w, lane4), ...);
+}
+template <int LOGB>
+__device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
+  pair_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 24>{});
+}
+
+__device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {
+  const uint4 v0 = lds128(a), v1 = lds128(a + 16), v2 = lds128(a + 32);
+  w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
+  w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+  w[8] = v2.x; w[9] = v2.y; w[10] = v2.z; w[11] = v2.w;
+}
+
+// ---- 2x box downsample of a 2 x 48-byte unit pair -> 24 output bytes --------
+// O = (a+b+c+d+2)>>2 computed bytewise without carries as
+//   (a>>2)+(b>>2)+(c>>2)+(d>>2) + (((a&3)+(b&3)+(c&3)+(d&3)+2)>>2)
+// which is exact (each term fits in its byte: 4*63+3 <= 255, 4*3+2 <= 255).
+template <int I>
+__device__ __forceinline__ uint32_t byte_of(const uint32_t* w) {
+  return (w[I >> 2] >> (8 * (I & 3))) & 0xFFu;
+}
+// output byte m (0..23) of the 8-pixel group: left source byte 2m - (m % 3), right = left + 3
+template <int M>
+struct DsIdx { static constexpr int L = 2 * M - (M % 3); static constexpr int R = L + 3; };
+
+template <int Q>
+__device__ __forceinline__ uint32_t ds_word(const uint32_t* t, const uint32_t* b) {
+  constexpr int m0 = 4 * Q, m1 = 4 * Q + 1, m2 = 4 * Q + 2, m3 = 4 * Q + 3;
+  const uint32_t TL = byte_of<DsIdx<m0>::L>(t) | byte_of<DsIdx<m1>::L>(t) << 8 | byte_of<DsIdx<m2>::L>(t) << 16 |
+                      byte_of<DsIdx<m3>::L>(t) << 24;
+  const uint32_t TR = byte_of<DsIdx<m0>::R>(t) | byte_of<DsIdx<m1>::R>(t) << 8 | byte_of<DsIdx<m2>::R>(t) << 16 |
+                      byte_of<DsIdx<m3>::R>(t) << 24;
+  const uint32_t BL = byte_of<DsIdx<m0>::L>(b) | byte_of<DsIdx<m1>::L>(b) << 8 | byte_of<DsIdx<m2>::L>(b) << 16 |
+                      byte_of<DsIdx<m3>::L>(b) << 24;
+  const uint32_t BR = byte_of<DsIdx<m0>::R>(b) | byte_of<DsIdx<m1>::R>(b) << 8 | byte_of<DsIdx<m2>::R>(b) << 16 |
+                      byte_of<DsIdx<m3>::R>(b) << 24;
+  const uint32_t hi = ((TL >> 2) & 0x3F3F3F3Fu) + ((TR >> 2) & 0x3F3F3F3Fu) + ((BL >> 2) & 0x3F3F3F3Fu) +
+                      ((BR >> 2) & 0x3F3F3F3Fu);
+  const uint32_t lo = (TL & 0x03030303u) + (TR & 0x03030303u) + (BL & 0x03030303u) + (BR & 0x03030303u) +
+                      0x02020202u;
+  return hi + ((lo >> 2) & 0x03030303u);
+}
+__device__ __forceinline__ void ds_unit(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+  o[0] = ds_word<0>(t, b); o[1] = ds_word<1>(t, b); o[2] = ds_word<2>(t, b);
+  o[3] = ds_word<3>(t, b); o[4] = ds_word<4>(t, b); o[5] = ds_word<5>(t, b);
+}
+__device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
+  uint2* d = reinterpret_cast<uint2*>(dst);
+  d[0] = make_uint2(o[0], o[1]);
+  d[1] = make_uint2(o[2], o[3]);
+  d[2] = make_uint2(o[4], o[5]);
+}
+
+// ---------------------------------------------------------------------------
+// The persistent TMA-ring histogram kernel. MODE 0: pair-key table (B = 2^LOGB
+// <= 16); MODE 1: single-key table, any B (LOGB unused); MODE 2: pair-key +
+// fused downsample.
+// ---------------------------------------------------------------------------
+template <int MODE, int LOGB>
+__global__ void __launch_bounds__(kThreads, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int BP = 1 << LOGB;
+  const uint32_t base = smem_addr(smem);
+  const Layout L = make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
+  uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
+  const int B = (MODE == 1) ? p.bins : BP;
+
+  if (threadIdx.x == 0) {
+    if (L.stages < 2) __trap();
+    for (int s = 0; s < L.stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsWarps);
+    }
+    fence_mbar_init();
+  }
+  // zero the table and the merge counters
+  for (uint32_t i = threadIdx.x; i < p.table_bytes / 16; i += kThreads) sts128(L.table + 16 * i, make_uint4(0, 0, 0, 0));
+  for (int i = threadIdx.x; i < 3 * 16; i += kThreads) hsum[i] = 0;
+  __syncthreads();
+
+  const int64_t t0 = p.total_tiles * blockIdx.x / gridDim.x;
+  const int64_t t1 = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
+
+  if (warp == kConsWarps) {
+    // ---------------- producer: one elected lane issues the bulk copies ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        const int64_t item = t / p.tpf;
+        const int32_t k = (int32_t)(t - item * p.tpf);
+        const uint64_t off = (uint64_t)k * p.tile;
+        const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
+        const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        mbar_arrive_expect_tx(full0 + 8 * s, bytes);
+        tma_load_1d(L.slot(s), reinterpret_cast<const void*>(frame_addr(p.src, item) + off), bytes, full0 + 8 * s);
+        if (++s == L.stages) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int ctid = threadIdx.x;  // 0 .. kConsThreads-1
+  const uint32_t lane4 = L.table | ((uint32_t)lane << 2);
+  int s = 0;
+  uint32_t ph = 0;
+  uint32_t rot = 0;  // rotates unit->thread assignment across tiles so all warps share the work
+  int64_t cur = -1;
+
+  auto out_row = [&](int64_t item) -> uint32_t* {
+    return item < p.n_halo ? p.halo_out + item * 3 * B : p.out + (item - p.n_halo) * 3 * B;
+  };
+
+  auto flush = [&](int64_t item) {
+    named_bar(kBarId, kConsThreads);
+    uint32_t* orow = out_row(item);
+    const int rows = (MODE == 1) ? 3 * B : 3 * BP * BP;
+    for (int r = ctid; r < rows; r += kConsThreads) {
+      const uint32_t ra = L.table + (uint32_t)r * 128u;
+      uint32_t sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t a = ra + (uint32_t)(((j + r) & 7) * 16);
+        const uint4 v = lds128(a);
+        sum += v.x + v.y + v.z + v.w;
+        sts128(a, make_uint4(0, 0, 0, 0));
+      }
+      if (sum) {
+        if (MODE == 1) {
+          red_global_add(orow + r, sum);
+        } else {
+          const int c = r / (BP * BP), key = r % (BP * BP);
+          atomicAdd(&hsum[c * BP + (key >> LOGB)], sum);
+          atomicAdd(&hsum[c * BP + (key & (BP - 1))], sum);
+        }
+      }
+    }
+    if (MODE != 1) {
+      named_bar(kBarId, kConsThreads);
+      if (ctid < 3 * BP) {
+        const uint32_t v = hsum[ctid];
+        hsum[ctid] = 0;
+        if (v) red_global_add(orow + ctid, v);
+      }
+    }
+    named_bar(kBarId, kConsThreads);
+  };
+
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t item = t / p.tpf;
+    const int32_t k = (int32_t)(t - item * p.tpf);
+    if (item != cur) {
+      if (cur >= 0) flush(cur);
+      cur = item;
+    }
+    const uint64_t off = (uint64_t)k * p.tile;
+    const uint32_t len = (uint32_t)((uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile);
+    mbar_wait(full0 + 8 * s, ph);
+    const uint32_t slot = L.slot(s);
+    const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
+
+    if constexpr (MODE == 2) {
+      // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs
+      const uint32_t rowb = (uint32_t)p.width * 3u;
+      const uint32_t upr = (uint32_t)p.width / 16u;
+      const uint32_t rows = len / rowb;
+      const uint32_t npairs = (rows / 2) * upr;
+      const int64_t ow3 = (int64_t)(p.width / 2) * 3;
+      uint8_t* dsf = (item >= p.n_halo)
+                         ? p.ds_out + (item - p.n_halo) * ((int64_t)(p.height / 2) * ow3) +
+                               ((int64_t)k * (p.rows_per_tile / 2)) * ow3
+                         : nullptr;
+      for (uint32_t u = first; u < npairs; u += kConsThreads) {
+        const uint32_t rp = u / upr, xc = u - rp * upr;
+        const uint32_t a = slot + rp * 2u * rowb + xc * 48u;
+        uint32_t wt[12], wb[12], o[6];
+        load_unit(a, wt);
+        load_unit(a + rowb, wb);
+        hist_unit_pair<LOGB>(wt, lane4);
+        hist_unit_pair<LOGB>(wb, lane4);
+        if (dsf) {
+          ds_unit(wt, wb, o);
+          st_global_24(dsf + (int64_t)rp * ow3 + xc * 24, o);
+        }
+      }
+      if (rows & 1) {  // odd last row of an odd-height frame: histogram only
+        for (uint32_t u = first; u < upr; u += kConsThreads) {
+          uint32_t w[12];
+          load_unit(slot + (rows - 1) * rowb + u * 48u, w);
+          hist_unit_pair<LOGB>(w, lane4);
+        }
+      }
+      rot = (rot + npairs) % kConsThreads;
+    } else {
+      const uint32_t nunits = len / 48u;
+      for (uint32_t u = first; u < nunits; u += kConsThreads) {
+        uint32_t w[12];
+        load_unit(slot + u * 48u, w);
+        if constexpr (MODE == 0) {
+          hist_unit_pair<LOGB>(w, lane4);
+        } else {
+          const uint32_t Bu = (uint32_t)B;
+#pragma unroll
+          for (int j = 0; j < 48; ++j) {
+            const uint32_t v = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+            const uint32_t bin = (v * Bu) >> 8;
+            red_shared_add(lane4 + (((uint32_t)(j % 3) * Bu + bin) << 7), 1u);
+          }
+        }
+      }
+      // tail bytes (frame size not a multiple of 48): direct global counts
+      const uint32_t rem = len - nunits * 48u;
+      if ((uint32_t)ctid < rem) {
+        const uint32_t j = nunits * 48u + (uint32_t)ctid;
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(slot + j));
+        const uint32_t bin = (v * (uint32_t)B) >> 8;
+        red_global_add(out_row(item) + (j % 3) * B + bin, 1u);
+      }
+      rot = (rot + nunits) % kConsThreads;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    if (++s == L.stages) { s = 0; ph ^= 1; }
+  }
+  if (cur >= 0) flush(cur);
+}
+
+// ---------------------------------------------------------------------------
+// K3: shot-diff. One warp per position.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) shotdiff_kernel(const uint32_t* __restrict__ hist,
+                                                        const uint32_t* __restrict__ halo,
+                                                        const uint8_t* __restrict__ seg, int64_t n, int32_t bins,
+                                                        uint32_t* __restrict__ diff) {
+  const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pos >= n) return;
+  const int K = 3 * bins;
+  uint32_t s = 0;
+  if (!seg[pos]) {
+    const uint32_t* cur = hist + pos * K;
+    const uint32_t* prev = pos == 0 ? halo : cur - K;
+    for (int i = lane; i < K; i += 32) {
+      const uint32_t a = cur[i], b = prev[i];
+      s += a > b ? a - b : b - a;
+    }
+  }
+  s = __reduce_add_sync(0xFFFFFFFFu, s);
+  if (lane == 0) diff[pos] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K4: downsample. Vectorised path (W % 16 == 0): one thread per 8 output pixels
+// from two 48-byte LDG.128 x3 loads; generic path: one thread per output byte.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ldg_unit(const uint8_t* p, uint32_t* w) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  const uint4 v0 = __ldcs(q), v1 = __ldcs(q + 1), v2 = __ldcs(q + 2);
+  w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
+  w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+  w[8] = v2.x; w[9] = v2.y; w[10] = v2.z; w[11] = v2.w;
+}
+
+__global__ void __launch_bounds__(256) downsample_vec_kernel(FrameSrc src, int64_t n, int32_t width, int32_t height,
+                                                             uint8_t* __restrict__ out) {
+  const int32_t upr = width / 16, oh = height / 2;
+  const int64_t units = (int64_t)upr * oh;
+  const int64_t rowb = (int64_t)width * 3, ow3 = (int64_t)(width / 2) * 3;
+  const int64_t total = units * n;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = g / units;
+    const int64_t u = g - item * units;
+    const int64_t y = u / upr, xc = u - y * upr;
+    const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item));
+    uint32_t wt[12], wb[12], o[6];
+    ldg_unit(f + 2 * y * rowb + xc * 48, wt);
+    ldg_unit(f + (2 * y + 1) * rowb + xc * 48, wb);
+    ds_unit(wt, wb, o);
+    st_global_24(out + item * (oh * ow3) + y * ow3 + xc * 24, o);
+  }
+}
+
+__global__ void __launch_bounds__(256) downsample_generic_kernel(FrameSrc src, int64_t n, int32_t width,
+                                                                 int32_t height, uint8_t* __restrict__ out) {
+  const int32_t ow = width / 2, oh = height / 2;
+  const int64_t per = (int64_t)ow * oh * 3;
+  const int64_t total = per * n;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = g / per;
+    const int64_t o = g - item * per;
+    const int64_t pix = o / 3;
+    const int c = (int)(o - pix * 3);
+    const int64_t y = pix / ow, x = pix - y * ow;
+    const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item));
+    const int64_t i00 = ((2 * y) * width + 2 * x) * 3 + c;
+    const uint32_t s = (uint32_t)f[i00] + f[i00 + 3] + f[i00 + (int64_t)width * 3] + f[i00 + (int64_t)width * 3 + 3];
+    out[g] = (uint8_t)((s + 2u) >> 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static int g_num_sms = 0;
+static int g_smem_optin = 0;
+
+static cudaError_t device_props() {
+  if (g_num_sms) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  return cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+}
+
+static int log2_exact(int b) {
+  for (int l = 0; l <= 4; ++l)
+    if ((1 << l) == b) return l;
+  return -1;
+}
+
+const char* hist_variant_name(int32_t bins) {
+  return log2_exact(bins) >= 0 ? "tma_pair_lane_private" : "tma_single_lane_private";
+}
+
+template <int MODE, int LOGB>
+static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
+  auto fn = hist_tma_kernel<MODE, LOGB>;
+  static int configured = 0;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    configured = 1;
+  }
+  int grid = g_num_sms;
+  if (p.total_tiles < grid) grid = (int)p.total_tiles;
+  if (grid < 1) return cudaSuccess;
+  fn<<<grid, kThreads, p.smem_bytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+static HistParams base_params(const HistJob& j) {
+  HistParams p{};
+  p.src = j.src;
+  p.n_items = j.n_items;
+  p.n_halo = j.n_halo;
+  p.out = j.out;
+  p.halo_out = j.halo_out;
+  p.ds_out = j.ds_out;
+  p.F = (int64_t)j.width * j.height * 3;
+  p.width = j.width;
+  p.height = j.height;
+  p.bins = j.bins;
+  p.smem_bytes = (uint32_t)g_smem_optin;
+  return p;
+}
+
+cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
+  cudaError_t e = device_props();
+  if (e != cudaSuccess) return e;
+  if (j.n_items <= 0) return cudaSuccess;
+  HistParams p = base_params(j);
+  p.ds_out = nullptr;
+  p.tile = kTile;
+  p.rows_per_tile = 0;
+  p.tpf = (int32_t)((p.F + kTile - 1) / kTile);
+  p.total_tiles = p.n_items * p.tpf;
+  const int lb = log2_exact(j.bins);
+  *launches += 1;
+  if (lb >= 0) {
+    const int Bp = 1 << lb;
+    p.table_bytes = 3u * Bp * Bp * 128u;
+    p.table_align = (uint32_t)Bp * Bp * 128u;
+    switch (lb) {
+      case 0: return launch_tma<0, 0>(p, st);
+      case 1: return launch_tma<0, 1>(p, st);
+      case 2: return launch_tma<0, 2>(p, st);
+      case 3: return launch_tma<0, 3>(p, st);
+      default: return launch_tma<0, 4>(p, st);
+    }
+  }
+  p.table_bytes = 3u * (uint32_t)j.bins * 128u;
+  p.table_align = 128u;
+  return launch_tma<1, 0>(p, st);
+}
+
+cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
+                              cudaStream_t st, int* launches) {
+  cudaError_t e = device_props();
+  if (e != cudaSuccess) return e;
+  if (n <= 0 || width < 2 || height < 2) return cudaSuccess;
+  *launches += 1;
+  const int grid = g_num_sms * 8;
+  if (width % 16 == 0) downsample_vec_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
+  else downsample_generic_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launches) {
+  cudaError_t e = device_props();
+  if (e != cudaSuccess) return e;
+  if (j.n_items <= 0) return cudaSuccess;
+  const int lb = log2_exact(j.bins);
+  const int64_t rowb = (int64_t)j.width * 3;
+  int rpt = (int)(kTile / rowb) & ~1;
+  if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
+  const bool fused = lb >= 0 && j.width % 16 == 0 && rpt >= 2 && j.n_halo == 0;
+  if (!fused) {
+    HistJob h = j;
+    h.ds_out = nullptr;
+    e = launch_histogram(h, st, launches);
+    if (e != cudaSuccess) return e;
+    FrameSrc src = j.src;
+    return launch_downsample(src, j.n_items, j.width, j.height, j.ds_out, st, launches);
+  }
+  HistParams p = base_params(j);
+  p.rows_per_tile = rpt;
+  p.tile = (uint32_t)(rpt * rowb);
+  p.tpf = (j.height + rpt - 1) / rpt;
+  p.total_tiles = p.n_items * p.tpf;
+  const int Bp = 1 << lb;
+  p.table_bytes = 3u * Bp * Bp * 128u;
+  p.table_align = (uint32_t)Bp * Bp * 128u;
+  *launches += 1;
+  switch (lb) {
+    case 0: return launch_tma<2, 0>(p, st);
+    case 1: return launch_tma<2, 1>(p, st);
+    case 2: return launch_tma<2, 2>(p, st);
+    case 3: return launch_tma<2, 3>(p, st);
+    default: return launch_tma<2, 4>(p, st);
+  }
+}
+
+cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
+                            int32_t bins, uint32_t* diff, cudaStream_t st, int* launches) {
+  if (n <= 0) return cudaSuccess;
+  *launches += 1;
+  const int64_t blocks = (n + 7) / 8;
+  shotdiff_kernel<<<(unsigned)blocks, 256, 0, st>>>(hist, halo_row, seg, n, bins, diff);
+  return cudaGetLastError();
+}
+
+}  // namespace scn

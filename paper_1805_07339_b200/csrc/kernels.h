@@ -1,0 +1,41 @@
+// kernels.h — internal launch interface between the C-ABI host code
+// (scn_api.cpp) and the sm_100a kernels (kernels.cu). Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace scn {
+
+// Where frame i of a launch lives: ptrs[i] if ptrs != nullptr, else base + i*stride.
+struct FrameSrc {
+  const uint64_t* ptrs;
+  uint64_t base;
+  uint64_t stride;
+};
+
+struct HistJob {
+  FrameSrc src;
+  int64_t n_items;     // frames in this launch
+  int32_t n_halo;      // the first n_halo items write to halo_out instead of out
+  uint32_t* out;       // [n_items - n_halo][3][bins]
+  uint32_t* halo_out;  // [n_halo][3][bins]
+  uint8_t* ds_out;     // fused downsample output [n_items - n_halo][H/2][W/2][3] or nullptr
+  int32_t width, height, bins;
+};
+
+// Histogram (zeroes nothing: the caller memsets out/halo_out first).
+// Returns the number of kernel launches in *launches.
+cudaError_t launch_histogram(const HistJob& job, cudaStream_t st, int* launches);
+// Fused HIST + downsample; falls back to two passes for shapes the fused kernel does not take.
+cudaError_t launch_hist_downsample(const HistJob& job, cudaStream_t st, int* launches);
+// Shot-diff over n positions; seg[p] != 0 marks a segment start; halo_row is the
+// histogram of the position before the first (used iff !seg[0]).
+cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
+                            int32_t bins, uint32_t* diff, cudaStream_t st, int* launches);
+cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
+                              cudaStream_t st, int* launches);
+
+// Variant names for reporting
+const char* hist_variant_name(int32_t bins);
+
+}  // namespace scn

@@ -1,0 +1,230 @@
+"""Harness shared by tests/, bench.py and __graft_entry__.smoke(): builds a
+workload's tables and sampled sequence through the product's C ABI, allocates
+device memory with torch, materialises only the sampled rows a shard needs
+(the paper's sparse decode: "only a sparse set ... must be
+computed"; here "decode" is the synthetic fill) and runs the hot path.
+
+It contains no histogram / difference / downsample arithmetic: every compute
+step goes through paper_1805_07339_b200 (libscn.so). The oracle is imported
+only by the callers that are allowed to use it (tests, smoke, bench baseline).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import paper_1805_07339_b200 as scn
+import scn_synth
+
+FAKE_BASE = 1 << 40  # placeholder (never dereferenced) for metadata-only planning tables
+
+
+def ceil16(x: int) -> int:
+    return (x + 15) & ~15
+
+
+def _sample(t, sampling):
+    kind = sampling[0]
+    if kind == "stride":
+        return scn.scn_sample_stride(t, sampling[1])
+    if kind == "range":
+        return scn.scn_sample_range(t, sampling[1], sampling[2])
+    if kind == "gather":
+        rows = scn_synth.gather_rows(sampling[1], scn.scn_table_rows(t), sampling[2])
+        return scn.scn_sample_gather(t, rows)
+    raise ValueError(kind)
+
+
+def _build_seq(wl: scn_synth.Workload, row_ptrs_of=None, where=scn.SCN_MEM_DEVICE):
+    """Create the per-video tables, sample each and concatenate.
+
+    row_ptrs_of(video) -> uint64[N] row pointers (sparse) or None (placeholder dense)."""
+    F16 = ceil16(wl.frame_bytes)
+    parts, tables = [], []
+    try:
+        for v in range(wl.n_videos):
+            if row_ptrs_of is None:
+                t = scn.scn_table_create(wl.rows_per_video, wl.width, wl.height, 3, where, FAKE_BASE, F16)
+            else:
+                t = scn.scn_table_create(wl.rows_per_video, wl.width, wl.height, 3, where, None, 0, row_ptrs_of(v))
+            tables.append(t)
+            parts.append(_sample(t, wl.sampling))
+        seq = scn.scn_seq_concat(parts) if len(parts) > 1 else parts.pop()
+    finally:
+        for p in parts:
+            scn.scn_seq_destroy(p)
+        for t in tables:
+            scn.scn_table_destroy(t)
+    return seq
+
+
+def plan(wl: scn_synth.Workload):
+    """Sampled positions of the whole job: (video[M], row[M], seg_start[M])."""
+    seq = _build_seq(wl)
+    try:
+        part, row = scn.scn_seq_rows(seq)
+        seg = scn.scn_seq_seg_starts(seq)
+    finally:
+        scn.scn_seq_destroy(seq)
+    return part.astype(np.int32), row, seg
+
+
+class DeviceJob:
+    """Positions [p0, p1) of a workload (plus the [-1,0] halo when asked) resident in HBM."""
+
+    def __init__(self, wl: scn_synth.Workload, p0: int, p1: int, with_halo: bool, spec: scn_synth.Spec | None = None,
+                 device="cuda", stream=None, plan_=None, buf: torch.Tensor | None = None):
+        self.wl = wl
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.part, self.row, self.seg = plan_ if plan_ is not None else plan(wl)
+        self.M = len(self.row)
+        self.p0, self.p1 = p0, p1
+        halo = 1 if (with_halo and 0 < p0 < self.M and not self.seg[p0]) else 0
+        self.lo = p0 - halo
+        self.F = wl.frame_bytes
+        self.F16 = ceil16(self.F)
+        n_mat = p1 - self.lo
+        need = max(n_mat, 1) * self.F16
+        if buf is not None and buf.numel() >= need:
+            self.buf = buf
+        else:
+            self.buf = torch.empty(need, dtype=torch.uint8, device=self.device)
+        base = self.buf.data_ptr()
+        addrs = base + np.arange(n_mat, dtype=np.uint64) * np.uint64(self.F16)
+        self.spec = spec if spec is not None else wl.spec()
+        if n_mat > 0:
+            jobs = torch.empty(n_mat * scn_synth.job_bytes(), dtype=torch.uint8, device=self.device)
+            with torch.cuda.stream(self.stream):
+                self.spec.fill_device(self.part[self.lo:p1], self.row[self.lo:p1], addrs, jobs.data_ptr(),
+                                      self.stream.cuda_stream)
+            self.stream.synchronize()
+            del jobs
+        # sparse tables: only positions [lo, p1) resident
+        ptrs = {}
+        for j in range(self.lo, p1):
+            v = int(self.part[j])
+            if v not in ptrs:
+                ptrs[v] = np.zeros(wl.rows_per_video, dtype=np.uint64)
+            ptrs[v][int(self.row[j])] = addrs[j - self.lo]
+        zeros = np.zeros(wl.rows_per_video, dtype=np.uint64)
+        self.seq = _build_seq(wl, lambda v: ptrs.get(v, zeros))
+        self.ws = torch.empty(max(scn.scn_seq_device_bytes(self.seq), 16), dtype=torch.uint8, device=self.device)
+        scn.scn_seq_upload(self.seq, self.ws, self.ws.numel(), self.stream)
+        self.stream.synchronize()
+
+    def alloc_outputs(self, ops=("hist", "shotdiff"), bins=None):
+        bins = bins or self.wl.bins
+        n = self.p1 - self.p0
+        out = {}
+        if "hist" in ops:
+            out["hist"] = torch.empty((max(n, 1), 3, bins), dtype=torch.int32, device=self.device)
+        if "shotdiff" in ops:
+            out["diff"] = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+            out["scratch"] = torch.empty(3 * bins, dtype=torch.int32, device=self.device)
+        if "downsample" in ops:
+            out["ds"] = torch.empty((max(n, 1), self.wl.height // 2, self.wl.width // 2, 3), dtype=torch.uint8,
+                                    device=self.device)
+        return out
+
+    def run(self, out, ops=("hist", "shotdiff"), bins=None, fused=True, stream=None):
+        """One pass of the hot path over [p0, p1) through the C ABI. Returns kernels launched."""
+        bins = bins or self.wl.bins
+        st = stream if stream is not None else self.stream
+        s, b, e = self.seq, self.p0, self.p1
+        launches = 0
+        if "hist" in ops and "shotdiff" in ops and fused:
+            scn.scn_run_hist_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
+            launches += scn.scn_last_launch_count()
+        elif "hist" in ops and "downsample" in ops and fused:
+            scn.scn_run_hist_downsample(s, b, e, bins, out["hist"], out["ds"], st)
+            launches += scn.scn_last_launch_count()
+            if "shotdiff" in ops:
+                scn.scn_run_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
+                launches += scn.scn_last_launch_count()
+        else:
+            if "hist" in ops:
+                scn.scn_run_histogram(s, b, e, bins, out["hist"], st)
+                launches += scn.scn_last_launch_count()
+            if "shotdiff" in ops:
+                scn.scn_run_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
+                launches += scn.scn_last_launch_count()
+            if "downsample" in ops:
+                scn.scn_run_downsample(s, b, e, out["ds"], st)
+                launches += scn.scn_last_launch_count()
+        return launches
+
+    def close(self):
+        if getattr(self, "seq", None) is not None:
+            scn.scn_seq_destroy(self.seq)
+            self.seq = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostJob:
+    """Positions [p0, p1) resident in pinned HOST memory (end-to-end path)."""
+
+    def __init__(self, wl: scn_synth.Workload, p0: int, p1: int, with_halo: bool, device="cuda", plan_=None,
+                 staging_frames: int = 32):
+        self.wl = wl
+        self.device = torch.device(device)
+        self.part, self.row, self.seg = plan_ if plan_ is not None else plan(wl)
+        self.M = len(self.row)
+        self.p0, self.p1 = p0, p1
+        halo = 1 if (with_halo and 0 < p0 < self.M and not self.seg[p0]) else 0
+        self.lo = p0 - halo
+        self.F = wl.frame_bytes
+        self.F16 = ceil16(self.F)
+        n_mat = p1 - self.lo
+        # generate on the device in chunks, copy into pinned host memory (generation is untimed)
+        self.host = torch.empty(max(n_mat, 1) * self.F16, dtype=torch.uint8, pin_memory=True)
+        chunk = max(1, min(n_mat, (1 << 31) // self.F16))
+        spec = wl.spec()
+        tmp = torch.empty(chunk * self.F16, dtype=torch.uint8, device=self.device)
+        jobs = torch.empty(chunk * scn_synth.job_bytes(), dtype=torch.uint8, device=self.device)
+        st = torch.cuda.current_stream(self.device)
+        for c0 in range(0, n_mat, chunk):
+            k = min(chunk, n_mat - c0)
+            addrs = tmp.data_ptr() + np.arange(k, dtype=np.uint64) * np.uint64(self.F16)
+            spec.fill_device(self.part[self.lo + c0:self.lo + c0 + k], self.row[self.lo + c0:self.lo + c0 + k],
+                             addrs, jobs.data_ptr(), st.cuda_stream)
+            self.host[c0 * self.F16:(c0 + k) * self.F16].copy_(tmp[:k * self.F16])
+        torch.cuda.synchronize(self.device)
+        del tmp, jobs
+        haddr = self.host.data_ptr() + np.arange(n_mat, dtype=np.uint64) * np.uint64(self.F16)
+        ptrs = {}
+        for j in range(self.lo, p1):
+            v = int(self.part[j])
+            if v not in ptrs:
+                ptrs[v] = np.zeros(wl.rows_per_video, dtype=np.uint64)
+            ptrs[v][int(self.row[j])] = haddr[j - self.lo]
+        zeros = np.zeros(wl.rows_per_video, dtype=np.uint64)
+        self.seq = _build_seq(wl, lambda v: ptrs.get(v, zeros), where=scn.SCN_MEM_HOST)
+        n = p1 - p0
+        self.staging_bytes = ceil16(max(n, 1)) + 2 * staging_frames * self.F16
+        self.staging = torch.empty(self.staging_bytes, dtype=torch.uint8, device=self.device)
+
+    def run(self, out, ops=("hist", "shotdiff"), bins=None, stream=None, copy_stream=None):
+        bins = bins or self.wl.bins
+        mask = ((scn.SCN_OP_HIST if "hist" in ops else 0) | (scn.SCN_OP_SHOTDIFF if "shotdiff" in ops else 0) |
+                (scn.SCN_OP_DOWNSAMPLE if "downsample" in ops else 0))
+        scn.scn_run_pipeline_host(self.seq, self.p0, self.p1, bins, mask, out.get("hist"), out.get("diff"),
+                                  out.get("ds"), out.get("scratch"), self.staging, self.staging_bytes, stream,
+                                  copy_stream)
+        return scn.scn_last_launch_count()
+
+    def close(self):
+        if getattr(self, "seq", None) is not None:
+            scn.scn_seq_destroy(self.seq)
+            self.seq = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,190 @@
+"""C-ABI host-side tests (no GPU): the library loads, exports every symbol
+include/scn.h declares, and its host logic (sampling P:L208, concatenation
+P:L181-185 / slices P:L216, shard math and halo P:L214, validation) agrees
+with the oracle and the header's error contract. No compute calls."""
+import ctypes
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1805_07339_b200 as scn
+import scn_harness
+import scn_synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAKE = 1 << 40
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "scn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(scn_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    syms = _declared_symbols()
+    assert len(syms) >= 20
+    lib = ctypes.CDLL(scn.LIB_PATH)
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert hasattr(scn, name), f"binding lacks {name}"
+
+
+def test_version_and_error_string():
+    assert "sm_100a" in scn.scn_version()
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_table_create(10, 0, 5, 3, scn.SCN_MEM_DEVICE, FAKE, 16)
+    assert e.value.status == scn.SCN_EINVAL
+    assert "width" in scn.scn_last_error()
+
+
+def _table(n, w=8, h=4):
+    F16 = (w * h * 3 + 15) & ~15
+    return scn.scn_table_create(n, w, h, 3, scn.SCN_MEM_DEVICE, FAKE, F16)
+
+
+def test_sampling_matches_oracle():
+    rng = random.Random(3)
+    for _ in range(300):
+        n = rng.randint(0, 80)
+        t = _table(n)
+        s = rng.randint(1, 90)
+        q = scn.scn_sample_stride(t, s)
+        assert scn.scn_seq_rows(q)[1].tolist() == oracle.sample_stride(n, s).tolist()
+        scn.scn_seq_destroy(q)
+        cuts = sorted(rng.sample(range(n + 1), k=min(n + 1, 2 * rng.randint(0, 3))))
+        blocks = [(cuts[i], cuts[i + 1]) for i in range(0, len(cuts) - 1, 2)]
+        k = rng.randint(1, 7)
+        q = scn.scn_sample_range(t, blocks, k)
+        assert scn.scn_seq_rows(q)[1].tolist() == oracle.sample_range(n, blocks, k).tolist()
+        scn.scn_seq_destroy(q)
+        rows = sorted(rng.sample(range(n), rng.randint(0, n))) if n else []
+        q = scn.scn_sample_gather(t, rows)
+        assert scn.scn_seq_rows(q)[1].tolist() == oracle.sample_gather(n, rows).tolist()
+        scn.scn_seq_destroy(q)
+        scn.scn_table_destroy(t)
+
+
+@pytest.mark.parametrize("call,status", [
+    (lambda t: scn.scn_sample_stride(t, 0), scn.SCN_EINVAL),
+    (lambda t: scn.scn_sample_gather(t, [4, 1]), scn.SCN_EINVAL),
+    (lambda t: scn.scn_sample_gather(t, [3, 3]), scn.SCN_EINVAL),
+    (lambda t: scn.scn_sample_gather(t, [10]), scn.SCN_ERANGE),
+    (lambda t: scn.scn_sample_gather(t, [-1]), scn.SCN_ERANGE),
+    (lambda t: scn.scn_sample_range(t, [(5, 8), (2, 4)], 1), scn.SCN_EINVAL),
+    (lambda t: scn.scn_sample_range(t, [(2, 11)], 1), scn.SCN_ERANGE),
+    (lambda t: scn.scn_sample_range(t, [(2, 5)], 0), scn.SCN_EINVAL),
+])
+def test_sampling_errors(call, status):
+    t = _table(10)
+    with pytest.raises(scn.ScnError) as e:
+        call(t)
+    assert e.value.status == status
+    scn.scn_table_destroy(t)
+
+
+def test_table_validation():
+    D = scn.SCN_MEM_DEVICE
+    bad = [
+        dict(num_rows=-1, width=8, height=4, base=FAKE, frame_stride_bytes=96),
+        dict(num_rows=4, width=8, height=4, channels=4, base=FAKE, frame_stride_bytes=96),
+        dict(num_rows=4, width=8, height=4, base=FAKE, frame_stride_bytes=95),   # < F
+        dict(num_rows=4, width=64, height=36, base=FAKE, frame_stride_bytes=6913),  # not multiple of 16
+        dict(num_rows=4, width=8, height=4, base=FAKE + 8, frame_stride_bytes=96),  # misaligned base
+        dict(num_rows=4, width=8, height=4),                                       # neither base nor rows
+        dict(num_rows=4, width=8, height=4, base=FAKE, frame_stride_bytes=96, row_ptrs=[16] * 4),  # both
+        dict(num_rows=2, width=8, height=4, row_ptrs=[16, 24]),                    # misaligned row ptr
+        dict(num_rows=1, width=40000, height=40000, base=FAKE, frame_stride_bytes=4800000000),  # W*H bound
+    ]
+    for kw in bad:
+        kw.setdefault("channels", 3)
+        with pytest.raises(scn.ScnError) as e:
+            scn.scn_table_create(where=D, **kw)
+        assert e.value.status == scn.SCN_EINVAL, kw
+    t = scn.scn_table_create(0, 8, 4, 3, D)  # empty table is valid (reading Q18)
+    q = scn.scn_sample_stride(t, 1)
+    assert scn.scn_seq_length(q) == 0
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)
+
+
+def test_concat_segments_and_halo():
+    ta, tb = _table(10), _table(7)
+    qa, qb = scn.scn_sample_stride(ta, 3), scn.scn_sample_stride(tb, 2)
+    q = scn.scn_seq_concat([qa, qb])
+    part, row = scn.scn_seq_rows(q)
+    assert part.tolist() == [0] * 4 + [1] * 4
+    assert row.tolist() == [0, 3, 6, 9, 0, 2, 4, 6]
+    assert scn.scn_seq_seg_starts(q).tolist() == [1, 0, 0, 0, 1, 0, 0, 0]
+    assert [scn.scn_seq_needs_halo(q, b) for b in range(9)] == [0, 1, 1, 1, 0, 1, 1, 1, 0]
+    t3 = scn.scn_table_create(5, 9, 4, 3, scn.SCN_MEM_DEVICE, FAKE, 112)
+    q3 = scn.scn_sample_stride(t3, 1)
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_seq_concat([qa, q3])  # unequal frame shape
+    assert e.value.status == scn.SCN_EINVAL
+    for x in (qa, qb, q, q3):
+        scn.scn_seq_destroy(x)
+    for t in (ta, tb, t3):
+        scn.scn_table_destroy(t)
+
+
+def test_shard_range():
+    for m in (0, 1, 7, 240, 16384, 36864):
+        for G in (1, 2, 3, 4, 8):
+            spans = [scn.scn_shard_range(m, G, r) for r in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(G - 1))
+            assert all(e - b in (m // G, m // G + 1) for b, e in spans)
+            assert spans == [((r * m) // G, ((r + 1) * m) // G) for r in range(G)]
+    for bad in ((10, 0, 0), (10, 2, 2), (10, 2, -1), (-1, 1, 0)):
+        with pytest.raises(scn.ScnError):
+            scn.scn_shard_range(*bad)
+
+
+def test_run_validation_without_gpu():
+    t = _table(10)
+    q = scn.scn_sample_stride(t, 1)
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_run_histogram(q, 0, 4, 0, 1 << 20)
+    assert e.value.status == scn.SCN_EUNSUPPORTED
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_run_histogram(q, 0, 11, 16, 1 << 20)
+    assert e.value.status == scn.SCN_ERANGE
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_run_histogram(q, 5, 4, 16, 1 << 20)
+    assert e.value.status == scn.SCN_EINVAL
+    with pytest.raises(scn.ScnError) as e:  # not uploaded
+        scn.scn_run_histogram(q, 0, 4, 16, 1 << 20)
+    assert e.value.status == scn.SCN_EINVAL
+    with pytest.raises(scn.ScnError) as e:  # device sequence on the host pipeline
+        scn.scn_run_pipeline_host(q, 0, 4, 16, 1, 1 << 20, None, None, None, 1 << 20, 1 << 20)
+    assert e.value.status == scn.SCN_EINVAL
+    scn.scn_run_histogram(q, 3, 3, 16, None)  # empty range is a no-op
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)
+
+
+@pytest.mark.parametrize("name", list(scn_synth.WORKLOADS))
+def test_plan_matches_oracle_sampling(name):
+    wl = scn_synth.WORKLOADS[name]
+    part, row, seg = scn_harness.plan(wl)
+    kind = wl.sampling[0]
+    per = []
+    for v in range(wl.n_videos):
+        if kind == "stride":
+            r = oracle.sample_stride(wl.rows_per_video, wl.sampling[1])
+        elif kind == "range":
+            r = oracle.sample_range(wl.rows_per_video, wl.sampling[1], wl.sampling[2])
+        else:
+            r = oracle.sample_gather(wl.rows_per_video,
+                                     scn_synth.gather_rows(wl.sampling[1], wl.rows_per_video, wl.sampling[2]))
+        per.append(r)
+    assert row.tolist() == np.concatenate(per).tolist()
+    assert part.tolist() == np.concatenate([[v] * len(r) for v, r in enumerate(per)]).tolist()
+    assert seg.sum() == wl.n_videos
+    expect_m = {"C1": 240, "C2": 16384, "C3": 36864, "C4": 4096, "C5": 7168}[name]
+    assert len(row) == expect_m
