@@ -288,7 +288,10 @@ def run_b200(args):
         ne = min(args.e2e_frames, M)
         eb, ee = scn.scn_shard_range(ne, world, rank)
         hj = scn_harness.HostJob(wl, eb, ee, with_halo=True, device=dev, plan_=plan_, staging_frames=48)
-        eo = job.alloc_outputs(("hist", "shotdiff"), bins)
+        ne_r = max(ee - eb, 1)
+        eo = {"hist": torch.empty((ne_r, 3, bins), dtype=torch.int32, device=dev),
+              "diff": torch.empty(ne_r, dtype=torch.int32, device=dev),
+              "scratch": torch.empty(3 * bins, dtype=torch.int32, device=dev)}
         h_hist = torch.empty((max(ee - eb, 1), 3, bins), dtype=torch.int32, pin_memory=True)
         h_diff = torch.empty(max(ee - eb, 1), dtype=torch.int32, pin_memory=True)
         cs = torch.cuda.Stream(dev)

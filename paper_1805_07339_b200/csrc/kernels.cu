@@ -34,13 +34,12 @@
 #include "ptx.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 namespace scn {
 
-constexpr int kConsWarps = 16;
-constexpr int kConsThreads = kConsWarps * 32;
-constexpr int kThreads = kConsThreads + 32;
+constexpr int kDefaultConsWarps = 16;  // consumer warps per CTA (+1 producer warp)
 constexpr uint32_t kTile = 30720;  // 640 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA)
 constexpr int kMaxStages = 8;
 constexpr uint32_t kCtrlBytes = 1024;
@@ -204,8 +203,11 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
 // <= 16); MODE 1: single-key table, any B (LOGB unused); MODE 2: pair-key +
 // fused downsample.
 // ---------------------------------------------------------------------------
-template <int MODE, int LOGB>
-__global__ void __launch_bounds__(kThreads, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
+template <int MODE, int LOGB, int NW>
+__global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
+  constexpr int kConsWarps = NW;
+  constexpr int kConsThreads = NW * 32;
+  constexpr int kThreads = kConsThreads + 32;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int BP = 1 << LOGB;
   const uint32_t base = smem_addr(smem);
@@ -477,9 +479,9 @@ const char* hist_variant_name(int32_t bins) {
   return log2_exact(bins) >= 0 ? "tma_pair_lane_private" : "tma_single_lane_private";
 }
 
-template <int MODE, int LOGB>
+template <int MODE, int LOGB, int NW = kDefaultConsWarps>
 static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
-  auto fn = hist_tma_kernel<MODE, LOGB>;
+  auto fn = hist_tma_kernel<MODE, LOGB, NW>;
   static int configured = 0;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
@@ -489,8 +491,25 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   int grid = g_num_sms;
   if (p.total_tiles < grid) grid = (int)p.total_tiles;
   if (grid < 1) return cudaSuccess;
-  fn<<<grid, kThreads, p.smem_bytes, st>>>(p);
+  fn<<<grid, NW * 32 + 32, p.smem_bytes, st>>>(p);
   return cudaGetLastError();
+}
+
+// Tuning knobs (env, read once): SCN_HIST_WARPS in {8,16,24} consumer warps for
+// the B=16 pair kernel, SCN_HIST_TILE tile bytes (multiple of 48). Defaults are
+// the measured best.
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+static int g_tune_warps = -1;
+static uint32_t g_tune_tile = 0;
+static void read_tuning() {
+  if (g_tune_warps >= 0) return;
+  g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
+  int t = env_int("SCN_HIST_TILE", (int)kTile);
+  if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
+  g_tune_tile = (uint32_t)t;
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -515,9 +534,10 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
   if (j.n_items <= 0) return cudaSuccess;
   HistParams p = base_params(j);
   p.ds_out = nullptr;
-  p.tile = kTile;
+  read_tuning();
+  p.tile = (j.bins == 16) ? g_tune_tile : kTile;
   p.rows_per_tile = 0;
-  p.tpf = (int32_t)((p.F + kTile - 1) / kTile);
+  p.tpf = (int32_t)((p.F + p.tile - 1) / p.tile);
   p.total_tiles = p.n_items * p.tpf;
   const int lb = log2_exact(j.bins);
   *launches += 1;
@@ -530,7 +550,10 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       case 1: return launch_tma<0, 1>(p, st);
       case 2: return launch_tma<0, 2>(p, st);
       case 3: return launch_tma<0, 3>(p, st);
-      default: return launch_tma<0, 4>(p, st);
+      default:
+        if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
+        if (g_tune_warps == 24) return launch_tma<0, 4, 24>(p, st);
+        return launch_tma<0, 4>(p, st);
     }
   }
   p.table_bytes = 3u * (uint32_t)j.bins * 128u;
