@@ -224,12 +224,7 @@ def run_b200(args):
     job = scn_harness.DeviceJob(wl, b, e, with_halo=True, spec=wl.spec(mode=args.mode), device=dev, stream=stream,
                                 plan_=plan_)
     out = job.alloc_outputs(("hist", "shotdiff"), bins)
-    rows_pad = -(-M // world)
-    if world > 1:
-        hist_pad = torch.zeros((rows_pad, 3, bins), dtype=torch.int32, device=dev)
-        diff_pad = torch.zeros(rows_pad, dtype=torch.int32, device=dev)
-        hist_all = torch.empty((rows_pad * world, 3, bins), dtype=torch.int32, device=dev)
-        diff_all = torch.empty(rows_pad * world, dtype=torch.int32, device=dev)
+    gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 else None
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     launches = [0]
@@ -243,11 +238,8 @@ def run_b200(args):
             ev[k][1].record(stream)
         scn.scn_run_shotdiff(job.seq, b, e, bins, out["hist"], out["diff"], out["scratch"], stream)
         launches[0] += scn.scn_last_launch_count()
-        if world > 1:
-            hist_pad[:n].copy_(out["hist"][:n])
-            diff_pad[:n].copy_(out["diff"][:n])
-            dist.all_gather_into_tensor(hist_all, hist_pad)
-            dist.all_gather_into_tensor(diff_all, diff_pad)
+        if gather is not None:
+            gather.gather(out["hist"], out["diff"], n)
         if k is not None:
             ev[k][2].record(stream)
 

@@ -4,8 +4,8 @@
 //
 // K1+K2 hist_pair_kernel<LOGB>  (bins = 2^LOGB <= 16; the configs' B = 16)
 //   Persistent, one CTA per SM (227 KB smem). Warp 16 is a TMA producer: one
-//   elected lane streams 30,720-byte tiles of the sampled frames with 1-D bulk
-//   copies (cp.async.bulk -> UBLKCP) into a 4-stage shared-memory ring guarded
+//   elected lane streams 43,008-byte tiles of the sampled frames with 1-D bulk
+//   copies (cp.async.bulk -> UBLKCP) into a 3-stage shared-memory ring guarded
 //   by full/empty mbarriers. Warps 0-15 consume: each thread takes 48-byte
 //   units (16 pixels, 3 x LDS.128, channel of byte j = j mod 3) and counts
 //   PAIRS of same-channel neighbours: key = (bin(a) << LOGB) | bin(b) into a
@@ -40,7 +40,8 @@
 namespace scn {
 
 constexpr int kDefaultConsWarps = 16;  // consumer warps per CTA (+1 producer warp)
-constexpr uint32_t kTile = 30720;  // 640 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA)
+constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
+                                   // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
 constexpr int kMaxStages = 8;
 constexpr uint32_t kCtrlBytes = 1024;
 constexpr uint32_t kBarId = 1;     // named barrier among consumer warps
@@ -70,30 +71,25 @@ __device__ __forceinline__ uint64_t frame_addr(const FrameSrc& s, int64_t i) {
 struct Layout {
   uint32_t ctrl;   // [full bars][empty bars][hsum]
   uint32_t table;
-  uint32_t gap_base, after_base, stride;
-  int n_gap, stages;
-  __device__ __forceinline__ uint32_t slot(int s) const {
-    return s < n_gap ? gap_base + (uint32_t)s * stride : after_base + (uint32_t)(s - n_gap) * stride;
-  }
+  uint32_t ring, stride;
+  int stages;
+  __device__ __forceinline__ uint32_t slot(int s) const { return ring + (uint32_t)s * stride; }
 };
 
-// Shared-memory layout: control block, then the lane-private table aligned to
-// table_align (so bin fields can be OR-ed into its address), tile slots in the
-// gap before the table and after it.
+// Shared-memory layout: 1 KB control block at the bottom, the lane-private table
+// at the highest table_align-aligned address that fits (so bin fields can be
+// OR-ed into its address), and one contiguous ring of tile slots in between.
 __device__ __forceinline__ Layout make_layout(uint32_t base, uint32_t smem_bytes, uint32_t tile, uint32_t tb_bytes,
                                               uint32_t tb_align) {
   Layout L;
   L.ctrl = base;
   const uint32_t end = base + smem_bytes;
-  const uint32_t t = (base + kCtrlBytes + tb_align - 1) & ~(tb_align - 1);
-  L.table = t;
+  L.table = (end - tb_bytes) & ~(tb_align - 1);
+  L.ring = (base + kCtrlBytes + 127) & ~127u;
   L.stride = (tile + 127) & ~127u;
-  L.gap_base = (base + kCtrlBytes + 127) & ~127u;
-  L.n_gap = t >= L.gap_base + tile ? (int)((t - L.gap_base - tile) / L.stride) + 1 : 0;
-  L.after_base = (t + tb_bytes + 127) & ~127u;
-  const int n_after = end >= L.after_base + tile ? (int)((end - L.after_base - tile) / L.stride) + 1 : 0;
-  L.stages = L.n_gap + n_after;
+  L.stages = L.table >= L.ring + tile ? (int)((L.table - L.ring - tile) / L.stride) + 1 : 0;
   if (L.stages > kMaxStages) L.stages = kMaxStages;
+  if (L.table < base + kCtrlBytes) L.stages = 0;
   return L;
 }
 
@@ -238,9 +234,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        const int64_t item = t / p.tpf;
-        const int32_t k = (int32_t)(t - item * p.tpf);
+      int64_t item = t0 / p.tpf;
+      int32_t k = (int32_t)(t0 - item * p.tpf);
+      for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
         const uint64_t off = (uint64_t)k * p.tile;
         const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
         const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
@@ -300,9 +296,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     named_bar(kBarId, kConsThreads);
   };
 
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t item = t / p.tpf;
-    const int32_t k = (int32_t)(t - item * p.tpf);
+  int64_t item = t0 / p.tpf;
+  int32_t k = (int32_t)(t0 - item * p.tpf);
+  for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
     if (item != cur) {
       if (cur >= 0) flush(cur);
       cur = item;
@@ -504,12 +500,16 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
+static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
   int t = env_int("SCN_HIST_TILE", (int)kTile);
   if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
   g_tune_tile = (uint32_t)t;
+  int f = env_int("SCN_FUSED_TILE", (int)kTile);
+  if (f < 96 || f > 65536) f = (int)kTile;
+  g_fused_tile = (uint32_t)f;
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -579,7 +579,8 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   if (j.n_items <= 0) return cudaSuccess;
   const int lb = log2_exact(j.bins);
   const int64_t rowb = (int64_t)j.width * 3;
-  int rpt = (int)(kTile / rowb) & ~1;
+  read_tuning();
+  int rpt = (int)(g_fused_tile / rowb) & ~1;
   if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
   const bool fused = lb >= 0 && j.width % 16 == 0 && rpt >= 2 && j.n_halo == 0;
   if (!fused) {

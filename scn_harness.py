@@ -228,3 +228,32 @@ class HostJob:
             self.close()
         except Exception:
             pass
+
+
+class ColumnGather:
+    """Final result exchange for N > 1: each rank's shard rows of
+    H [n,3,B] and D [n] are padded to ceil(M/G) rows and all-gathered (NCCL on the
+    GPU box, gloo in the CPU tests); result() trims the padding back out."""
+
+    def __init__(self, M: int, world: int, bins: int, device, dist):
+        self.M, self.world, self.bins, self.dist = M, world, bins, dist
+        self.rows_pad = -(-M // world) if world else 0
+        self.spans = [scn.scn_shard_range(M, world, r) for r in range(world)]
+        self.hist_pad = torch.zeros((self.rows_pad, 3, bins), dtype=torch.int32, device=device)
+        self.diff_pad = torch.zeros(self.rows_pad, dtype=torch.int32, device=device)
+        self.hist_all = torch.empty((self.rows_pad * world, 3, bins), dtype=torch.int32, device=device)
+        self.diff_all = torch.empty(self.rows_pad * world, dtype=torch.int32, device=device)
+
+    def gather(self, hist, diff, n: int):
+        self.hist_pad[:n].copy_(hist[:n])
+        self.diff_pad[:n].copy_(diff[:n])
+        self.dist.all_gather_into_tensor(self.hist_all, self.hist_pad)
+        self.dist.all_gather_into_tensor(self.diff_all, self.diff_pad)
+
+    def result(self):
+        hs, ds = [], []
+        for r, (b, e) in enumerate(self.spans):
+            o = r * self.rows_pad
+            hs.append(self.hist_all[o:o + e - b])
+            ds.append(self.diff_all[o:o + e - b])
+        return torch.cat(hs), torch.cat(ds)
