@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline budget (oracle, rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames-per-step", type=int, default=16)
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
     return ap.parse_args()
 
 
@@ -208,10 +209,14 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev_index = local % max(torch.cuda.device_count(), 1)  # == local on a multi-GPU box
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     wl = scn_synth.WORKLOADS[args.config]
     plan_ = scn_harness.plan(wl)
@@ -250,7 +255,7 @@ def run_b200(args):
         dist.barrier()
     launches[0] = 0
     props = torch.cuda.get_device_properties(dev)
-    gpu_id = f"GPU-{props.uuid}" if getattr(props, "uuid", None) else str(local)
+    gpu_id = f"GPU-{props.uuid}" if getattr(props, "uuid", None) else str(dev_index)
     clocks = ClockSampler(gpu_id)
     clocks.start()
     time.sleep(0.3)

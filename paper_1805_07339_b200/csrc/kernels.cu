@@ -111,11 +111,13 @@ __device__ __forceinline__ uint32_t bin_field(const uint32_t* w) {
 }
 
 // Byte J of the unit shifted so its top LOGB bits (its bin) land at bit DST (unmasked).
-template <int J, int DST, int LOGB>
+// VAR 1 moves right shifts to the FMA pipe (mul.hi by 2^(32-s)), balancing ALU and FMA.
+template <int J, int DST, int LOGB, int VAR = 0>
 __device__ __forceinline__ uint32_t bin_shift(const uint32_t* w) {
   constexpr int src = 8 * (J & 3) + 8 - LOGB;
   const uint32_t x = w[J >> 2];
-  if constexpr (src >= DST) return x >> (src - DST);
+  if constexpr (src > DST && VAR == 1) return __umulhi(x, 1u << (32 - (src - DST)));
+  else if constexpr (src >= DST) return x >> (src - DST);
   else return x << (DST - src);
 }
 // (a & b) | c in one LOP3
@@ -128,23 +130,23 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
 
 // Count the 24 same-channel pixel pairs of one 48-byte unit (16 pixels).
 // lane4 = table base | lane << 2. Pair (2q, 2q+1) of channel c: bytes 6q+c, 6q+3+c.
-template <int LOGB, int P>
+template <int LOGB, int P, int VAR = 0>
 __device__ __forceinline__ void pair_unit_step(const uint32_t* w, uint32_t lane4) {
   constexpr int q = P / 3, c = P % 3;
   constexpr int JA = 6 * q + c, JB = 6 * q + 3 + c;
   constexpr int B = 1 << LOGB;
   // addr = (yA & maskA) | ((yB & maskB) | lane4): two LOP3s (forced; the compiler emits three)
-  const uint32_t lo = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<JB, 7, LOGB>(w), lane4);
-  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << (7 + LOGB)>(bin_shift<JA, 7 + LOGB, LOGB>(w), lo);
+  const uint32_t lo = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<JB, 7, LOGB, VAR>(w), lane4);
+  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << (7 + LOGB)>(bin_shift<JA, 7 + LOGB, LOGB, VAR>(w), lo);
   red_shared_add_off<c * B * B * 128>(addr);
 }
-template <int LOGB, int... P>
+template <int LOGB, int VAR, int... P>
 __device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
-  (pair_unit_step<LOGB, P>(w, lane4), ...);
+  (pair_unit_step<LOGB, P, VAR>(w, lane4), ...);
 }
-template <int LOGB>
+template <int LOGB, int VAR = 0>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
-  pair_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 24>{});
+  pair_unit_all<LOGB, VAR & 1>(w, lane4, std::make_integer_sequence<int, 24>{});
 }
 
 __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {
@@ -199,7 +201,7 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
 // <= 16); MODE 1: single-key table, any B (LOGB unused); MODE 2: pair-key +
 // fused downsample.
 // ---------------------------------------------------------------------------
-template <int MODE, int LOGB, int NW>
+template <int MODE, int LOGB, int NW, int VAR = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
   constexpr int kConsWarps = NW;
   constexpr int kConsThreads = NW * 32;
@@ -343,11 +345,22 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       rot = (rot + npairs) % kConsThreads;
     } else {
       const uint32_t nunits = len / 48u;
-      for (uint32_t u = first; u < nunits; u += kConsThreads) {
+      uint32_t u0 = first;
+      if constexpr (MODE == 0 && (VAR & 2)) {
+        // two units per iteration: 6 LDS.128 in flight, 48 independent atomics
+        for (; u0 + kConsThreads < nunits; u0 += 2 * kConsThreads) {
+          uint32_t w[12], w2[12];
+          load_unit(slot + u0 * 48u, w);
+          load_unit(slot + (u0 + kConsThreads) * 48u, w2);
+          hist_unit_pair<LOGB, VAR>(w, lane4);
+          hist_unit_pair<LOGB, VAR>(w2, lane4);
+        }
+      }
+      for (uint32_t u = u0; u < nunits; u += kConsThreads) {
         uint32_t w[12];
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == 0) {
-          hist_unit_pair<LOGB>(w, lane4);
+          hist_unit_pair<LOGB, VAR>(w, lane4);
         } else {
           const uint32_t Bu = (uint32_t)B;
 #pragma unroll
@@ -475,9 +488,9 @@ const char* hist_variant_name(int32_t bins) {
   return log2_exact(bins) >= 0 ? "tma_pair_lane_private" : "tma_single_lane_private";
 }
 
-template <int MODE, int LOGB, int NW = kDefaultConsWarps>
+template <int MODE, int LOGB, int NW = kDefaultConsWarps, int VAR = 0>
 static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
-  auto fn = hist_tma_kernel<MODE, LOGB, NW>;
+  auto fn = hist_tma_kernel<MODE, LOGB, NW, VAR>;
   static int configured = 0;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
@@ -500,7 +513,8 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
-static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
+static uint32_t g_fused_tile = 0;
+static int g_tune_var = 0;  // SCN_HIST_VAR: 1 = mul.hi shifts, 2 = two units/iteration, 3 = both  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -510,6 +524,7 @@ static void read_tuning() {
   int f = env_int("SCN_FUSED_TILE", (int)kTile);
   if (f < 96 || f > 65536) f = (int)kTile;
   g_fused_tile = (uint32_t)f;
+  g_tune_var = env_int("SCN_HIST_VAR", 0);
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -553,6 +568,9 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       default:
         if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
         if (g_tune_warps == 24) return launch_tma<0, 4, 24>(p, st);
+        if (g_tune_var == 1) return launch_tma<0, 4, 16, 1>(p, st);
+        if (g_tune_var == 2) return launch_tma<0, 4, 16, 2>(p, st);
+        if (g_tune_var == 3) return launch_tma<0, 4, 16, 3>(p, st);
         return launch_tma<0, 4>(p, st);
     }
   }

@@ -247,6 +247,15 @@ class ColumnGather:
     def gather(self, hist, diff, n: int):
         self.hist_pad[:n].copy_(hist[:n])
         self.diff_pad[:n].copy_(diff[:n])
+        if self.hist_pad.is_cuda and self.dist.get_backend() == "gloo":
+            # test-only path (several ranks sharing one GPU): gloo gathers host copies
+            hp, dp = self.hist_pad.cpu(), self.diff_pad.cpu()
+            ha, da = self.hist_all.cpu(), self.diff_all.cpu()
+            self.dist.all_gather_into_tensor(ha, hp)
+            self.dist.all_gather_into_tensor(da, dp)
+            self.hist_all.copy_(ha)
+            self.diff_all.copy_(da)
+            return
         self.dist.all_gather_into_tensor(self.hist_all, self.hist_pad)
         self.dist.all_gather_into_tensor(self.diff_all, self.diff_pad)
 

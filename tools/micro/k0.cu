@@ -160,7 +160,26 @@ static double median_cycles(std::vector<long long>& c) {
 }
 #include <algorithm>
 
-int main() {
+static int sustained(int reps) {
+  // sustained TMA read (tile 43008, 3 stages, 17 warps) of 48 GB, reps times: is the HBM side stable?
+  int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  size_t bytes = (size_t)48 << 30; uint8_t* buf; CK(cudaMalloc(&buf, bytes)); CK(cudaMemset(buf, 1, bytes));
+  uint32_t* dout; CK(cudaMalloc(&dout, 64));
+  uint32_t tile = 43008; int stages = 3; size_t smem = 256 + (size_t)stages * tile; size_t ntiles = bytes / tile;
+  CK(cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  printf("{\"sustained_tma_read_GBps\": [");
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0); k_tma<<<nsm, 17 * 32, smem>>>(buf, ntiles, tile, stages, dout); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("%s%.0f", r ? ", " : "", (double)ntiles * tile / (ms * 1e6));
+  }
+  printf("]}\n");
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return sustained(atoi(argv[1]));
   int dev = 0; CK(cudaSetDevice(dev));
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, dev));
   const int nsm = prop.multiProcessorCount;
