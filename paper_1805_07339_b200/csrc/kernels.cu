@@ -42,6 +42,7 @@ namespace scn {
 constexpr int kDefaultConsWarps = 16;  // consumer warps per CTA (+1 producer warp)
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
                                    // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
+constexpr uint32_t kFusedTile = 64512;  // target bytes per row-pair tile of the downsample kernels (measured)
 constexpr int kMaxStages = 8;
 constexpr uint32_t kCtrlBytes = 1024;
 constexpr uint32_t kBarId = 1;     // named barrier among consumer warps
@@ -185,10 +186,68 @@ __device__ __forceinline__ uint32_t ds_word(const uint32_t* t, const uint32_t* b
                       0x02020202u;
   return hi + ((lo >> 2) & 0x03030303u);
 }
-__device__ __forceinline__ void ds_unit(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+// Reference formulation (kept for readability; ds_unit below is the fast path).
+__device__ __forceinline__ void ds_unit_bytewise(const uint32_t* t, const uint32_t* b, uint32_t* o) {
   o[0] = ds_word<0>(t, b); o[1] = ds_word<1>(t, b); o[2] = ds_word<2>(t, b);
   o[3] = ds_word<3>(t, b); o[4] = ds_word<4>(t, b); o[5] = ds_word<5>(t, b);
 }
+
+// Fast 2x2 average of 16 pixels x 2 rows (t, b: 12 words each) -> 8 pixels (6 words).
+// Per word: vertical partial sums of the high 6 bits (hv) and low 2 bits (lv) of
+// each byte; a funnel shift by 3 bytes aligns pixel 2x+1 over pixel 2x, so
+// A = hv + hv>>24b + (((lv + lv>>24b + 2) >> 2) & 3) is the exact average at every
+// byte position p with p mod 6 in {0,1,2}; ten PRMTs compact those bytes.
+__device__ __forceinline__ void ds_unit(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+  uint32_t hv[13], lv[13], A[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    hv[k] = ((t[k] >> 2) & 0x3F3F3F3Fu) + ((b[k] >> 2) & 0x3F3F3F3Fu);  // <= 126 per byte
+    lv[k] = (t[k] & 0x03030303u) + (b[k] & 0x03030303u);                // <= 6 per byte
+  }
+  hv[12] = 0;
+  lv[12] = 0;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const uint32_t H = hv[k] + __funnelshift_r(hv[k], hv[k + 1], 24);               // <= 252
+    const uint32_t Lo = lv[k] + __funnelshift_r(lv[k], lv[k + 1], 24) + 0x02020202u;  // <= 14
+    A[k] = H + ((Lo >> 2) & 0x03030303u);                                            // <= 255
+  }
+  // output byte m <- stream byte 2m - (m mod 3)
+  o[0] = __byte_perm(A[0], A[1], 0x6210);
+  o[1] = __byte_perm(__byte_perm(A[1], A[2], 0x0043), A[3], 0x5410);
+  o[2] = __byte_perm(__byte_perm(A[3], A[4], 0x0762), A[5], 0x4210);
+  o[3] = __byte_perm(A[6], A[7], 0x6210);
+  o[4] = __byte_perm(__byte_perm(A[7], A[8], 0x0043), A[9], 0x5410);
+  o[5] = __byte_perm(__byte_perm(A[9], A[10], 0x0762), A[11], 0x4210);
+}
+// dp4a variant: output byte m = (T_i + T_{i+3} + B_i + B_{i+3} + 2) >> 2 with i = 2m - m%3,
+// each pair taken from a 4-byte window (funnel shift) by one IDP.4A with weights
+// (1,0,0,1); the sums run on the FMA pipe instead of the ALU pipe.
+template <int I>
+__device__ __forceinline__ uint32_t win4(const uint32_t* w) {
+  if constexpr ((I & 3) == 0) return w[I >> 2];
+  else return __funnelshift_r(w[I >> 2], w[(I >> 2) + 1], 8 * (I & 3));
+}
+template <int M>
+__device__ __forceinline__ uint32_t ds_sum(const uint32_t* t, const uint32_t* b) {
+  constexpr int I = 2 * M - (M % 3);
+  return __dp4a(win4<I>(b), 0x01000001u, __dp4a(win4<I>(t), 0x01000001u, 2u)) >> 2;
+}
+template <int Q>
+__device__ __forceinline__ uint32_t ds_word4(const uint32_t* t, const uint32_t* b) {
+  return ds_sum<4 * Q>(t, b) | ds_sum<4 * Q + 1>(t, b) << 8 | ds_sum<4 * Q + 2>(t, b) << 16 |
+         ds_sum<4 * Q + 3>(t, b) << 24;
+}
+__device__ __forceinline__ void ds_unit_dp4a(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+  o[0] = ds_word4<0>(t, b); o[1] = ds_word4<1>(t, b); o[2] = ds_word4<2>(t, b);
+  o[3] = ds_word4<3>(t, b); o[4] = ds_word4<4>(t, b); o[5] = ds_word4<5>(t, b);
+}
+template <int DSV>
+__device__ __forceinline__ void ds_unit_v(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+  if constexpr (DSV == 1) ds_unit_dp4a(t, b, o);
+  else ds_unit(t, b, o);
+}
+
 __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
   uint2* d = reinterpret_cast<uint2*>(dst);
   d[0] = make_uint2(o[0], o[1]);
@@ -199,7 +258,7 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
 // ---------------------------------------------------------------------------
 // The persistent TMA-ring histogram kernel. MODE 0: pair-key table (B = 2^LOGB
 // <= 16); MODE 1: single-key table, any B (LOGB unused); MODE 2: pair-key +
-// fused downsample.
+// fused downsample; MODE 3: downsample only (no table). VAR bit 2: dp4a downsample.
 // ---------------------------------------------------------------------------
 template <int MODE, int LOGB, int NW, int VAR = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
@@ -264,6 +323,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   };
 
   auto flush = [&](int64_t item) {
+    if constexpr (MODE == 3) return;
     named_bar(kBarId, kConsThreads);
     uint32_t* orow = out_row(item);
     const int rows = (MODE == 1) ? 3 * B : 3 * BP * BP;
@@ -311,7 +371,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const uint32_t slot = L.slot(s);
     const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
-    if constexpr (MODE == 2) {
+    if constexpr (MODE >= 2) {
       // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs
       const uint32_t rowb = (uint32_t)p.width * 3u;
       const uint32_t upr = (uint32_t)p.width / 16u;
@@ -328,14 +388,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         uint32_t wt[12], wb[12], o[6];
         load_unit(a, wt);
         load_unit(a + rowb, wb);
-        hist_unit_pair<LOGB>(wt, lane4);
-        hist_unit_pair<LOGB>(wb, lane4);
+        if constexpr (MODE == 2) {
+          hist_unit_pair<LOGB>(wt, lane4);
+          hist_unit_pair<LOGB>(wb, lane4);
+        }
         if (dsf) {
-          ds_unit(wt, wb, o);
+          ds_unit_v<(VAR >> 2) & 1>(wt, wb, o);
           st_global_24(dsf + (int64_t)rp * ow3 + xc * 24, o);
         }
       }
-      if (rows & 1) {  // odd last row of an odd-height frame: histogram only
+      if (MODE == 2 && (rows & 1)) {  // odd last row of an odd-height frame: histogram only
         for (uint32_t u = first; u < upr; u += kConsThreads) {
           uint32_t w[12];
           load_unit(slot + (rows - 1) * rowb + u * 48u, w);
@@ -425,22 +487,21 @@ __device__ __forceinline__ void ldg_unit(const uint8_t* p, uint32_t* w) {
   w[8] = v2.x; w[9] = v2.y; w[10] = v2.z; w[11] = v2.w;
 }
 
-__global__ void __launch_bounds__(256) downsample_vec_kernel(FrameSrc src, int64_t n, int32_t width, int32_t height,
-                                                             uint8_t* __restrict__ out) {
-  const int32_t upr = width / 16, oh = height / 2;
-  const int64_t units = (int64_t)upr * oh;
-  const int64_t rowb = (int64_t)width * 3, ow3 = (int64_t)(width / 2) * 3;
-  const int64_t total = units * n;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = g / units;
-    const int64_t u = g - item * units;
-    const int64_t y = u / upr, xc = u - y * upr;
-    const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item));
-    uint32_t wt[12], wb[12], o[6];
-    ldg_unit(f + 2 * y * rowb + xc * 48, wt);
-    ldg_unit(f + (2 * y + 1) * rowb + xc * 48, wb);
-    ds_unit(wt, wb, o);
-    st_global_24(out + item * (oh * ow3) + y * ow3 + xc * 24, o);
+// one block per (output row y = blockIdx.x, frame = item0 + blockIdx.y); threads over 48-byte column units
+__global__ void __launch_bounds__(128) downsample_vec_kernel(FrameSrc src, int64_t item0, int32_t width,
+                                                             int32_t height, uint8_t* __restrict__ out) {
+  const uint32_t upr = (uint32_t)width / 16u, oh = (uint32_t)height / 2u;
+  const uint32_t y = blockIdx.x;
+  const int64_t item = item0 + blockIdx.y;
+  const uint32_t rowb = (uint32_t)width * 3u, ow3 = (uint32_t)(width / 2) * 3u;
+  const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item)) + (size_t)(2u * y) * rowb;
+  uint8_t* o = out + item * ((int64_t)oh * ow3) + (int64_t)y * ow3;
+  for (uint32_t xc = threadIdx.x; xc < upr; xc += blockDim.x) {
+    uint32_t wt[12], wb[12], r[6];
+    ldg_unit(f + xc * 48u, wt);
+    ldg_unit(f + rowb + xc * 48u, wb);
+    ds_unit(wt, wb, r);
+    st_global_24(o + xc * 24u, r);
   }
 }
 
@@ -514,17 +575,21 @@ static int env_int(const char* name, int dflt) {
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
 static uint32_t g_fused_tile = 0;
-static int g_tune_var = 0;  // SCN_HIST_VAR: 1 = mul.hi shifts, 2 = two units/iteration, 3 = both  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
+static int g_tune_var = 0;  // SCN_HIST_VAR: 1 = mul.hi shifts, 2 = two units/iteration, 3 = both
+static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
+static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
   int t = env_int("SCN_HIST_TILE", (int)kTile);
   if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
   g_tune_tile = (uint32_t)t;
-  int f = env_int("SCN_FUSED_TILE", (int)kTile);
+  int f = env_int("SCN_FUSED_TILE", (int)kFusedTile);
   if (f < 96 || f > 65536) f = (int)kTile;
   g_fused_tile = (uint32_t)f;
   g_tune_var = env_int("SCN_HIST_VAR", 0);
+  g_ds_var = env_int("SCN_DS_VAR", 1);
+  g_ds_impl = env_int("SCN_DS_IMPL", 0);
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -579,15 +644,32 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
   return launch_tma<1, 0>(p, st);
 }
 
+static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
+                                 cudaStream_t st);
+
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
                               cudaStream_t st, int* launches) {
   cudaError_t e = device_props();
   if (e != cudaSuccess) return e;
   if (n <= 0 || width < 2 || height < 2) return cudaSuccess;
-  *launches += 1;
-  const int grid = g_num_sms * 8;
-  if (width % 16 == 0) downsample_vec_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
-  else downsample_generic_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
+  read_tuning();
+  if (width % 16 == 0 && g_ds_impl == 0 && (int64_t)width * 6 <= 65536) {
+    *launches += 1;
+    return launch_ds_tma(src, n, width, height, out, st);
+  }
+  if (width % 16 == 0) {
+    *launches += (int)((n + 65534) / 65535);
+    const int threads = width / 16 >= 128 ? 128 : ((width / 16 + 31) / 32) * 32;
+    for (int64_t i0 = 0; i0 < n; i0 += 65535) {
+      const int64_t cnt = n - i0 < 65535 ? n - i0 : 65535;
+      dim3 grid((unsigned)(height / 2), (unsigned)cnt);
+      downsample_vec_kernel<<<grid, threads, 0, st>>>(src, i0, width, height, out);
+    }
+  } else {
+    *launches += 1;
+    const int grid = g_num_sms * 8;
+    downsample_generic_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
+  }
   return cudaGetLastError();
 }
 
@@ -623,8 +705,34 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     case 1: return launch_tma<2, 1>(p, st);
     case 2: return launch_tma<2, 2>(p, st);
     case 3: return launch_tma<2, 3>(p, st);
-    default: return launch_tma<2, 4>(p, st);
+    default:
+      if (g_ds_var == 1) return launch_tma<2, 4, kDefaultConsWarps, 4>(p, st);
+      return launch_tma<2, 4>(p, st);
   }
+}
+
+// downsample-only TMA ring (MODE 3): same row-pair tiles, no table
+static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
+                                 cudaStream_t st) {
+  HistJob j{};
+  j.src = src;
+  j.n_items = n;
+  j.ds_out = out;
+  j.width = width;
+  j.height = height;
+  j.bins = 16;
+  HistParams p = base_params(j);
+  const int64_t rowb = (int64_t)width * 3;
+  int rpt = (int)(g_fused_tile / rowb) & ~1;
+  if (rpt > height) rpt = height + (height & 1);
+  p.rows_per_tile = rpt;
+  p.tile = (uint32_t)(rpt * rowb);
+  p.tpf = (height + rpt - 1) / rpt;
+  p.total_tiles = n * p.tpf;
+  p.table_bytes = 0;
+  p.table_align = 128;
+  if (g_ds_var == 1) return launch_tma<3, 4, kDefaultConsWarps, 4>(p, st);
+  return launch_tma<3, 4>(p, st);
 }
 
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
