@@ -107,14 +107,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profile(frames: int, F: int):
+def traffic_from_profile(frames: int, F: int, kernel: str = "hist"):
     """dram bytes per launch from the committed ncu --set full summary (bytes/frame x frames), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_hist_summary.json")
+    p = os.path.join(ROOT, "profiles", f"ncu_{kernel}_summary.json")
     if not os.path.exists(p):
         return None, None
     d = json.load(open(p))
     bpf = d.get("dram_bytes_per_frame")
-    if not bpf or d.get("frame_bytes") != F:
+    if not bpf or d.get("frame_bytes") != F or d.get("kernel") != kernel:
         return None, None
     return float(bpf) * frames, d.get("source", p)
 
@@ -228,7 +228,9 @@ def run_b200(args):
     stream = torch.cuda.current_stream(dev)
     job = scn_harness.DeviceJob(wl, b, e, with_halo=True, spec=wl.spec(mode=args.mode), device=dev, stream=stream,
                                 plan_=plan_)
-    out = job.alloc_outputs(("hist", "shotdiff"), bins)
+    do_diff, do_ds = "shotdiff" in wl.ops, "downsample" in wl.ops
+    ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
+    out = job.alloc_outputs(ops, bins)
     gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 else None
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
@@ -237,14 +239,18 @@ def run_b200(args):
     def step(k=None):
         if k is not None:
             ev[k][0].record(stream)
-        scn.scn_run_histogram(job.seq, b, e, bins, out["hist"], stream)
+        if do_ds:  # HIST + 2x downsample in one read of each frame (reading Q12)
+            scn.scn_run_hist_downsample(job.seq, b, e, bins, out["hist"], out["ds"], stream)
+        else:
+            scn.scn_run_histogram(job.seq, b, e, bins, out["hist"], stream)
         launches[0] += scn.scn_last_launch_count()
         if k is not None:
             ev[k][1].record(stream)
-        scn.scn_run_shotdiff(job.seq, b, e, bins, out["hist"], out["diff"], out["scratch"], stream)
-        launches[0] += scn.scn_last_launch_count()
+        if do_diff:
+            scn.scn_run_shotdiff(job.seq, b, e, bins, out["hist"], out["diff"], out["scratch"], stream)
+            launches[0] += scn.scn_last_launch_count()
         if gather is not None:
-            gather.gather(out["hist"], out["diff"], n)
+            gather.gather(out["hist"], out.get("diff"), n)
         if k is not None:
             ev[k][2].record(stream)
 
@@ -289,14 +295,16 @@ def run_b200(args):
         eo = {"hist": torch.empty((ne_r, 3, bins), dtype=torch.int32, device=dev),
               "diff": torch.empty(ne_r, dtype=torch.int32, device=dev),
               "scratch": torch.empty(3 * bins, dtype=torch.int32, device=dev)}
-        h_hist = torch.empty((max(ee - eb, 1), 3, bins), dtype=torch.int32, pin_memory=True)
-        h_diff = torch.empty(max(ee - eb, 1), dtype=torch.int32, pin_memory=True)
+        if do_ds:
+            eo["ds"] = torch.empty((ne_r, wl.height // 2, wl.width // 2, 3), dtype=torch.uint8, device=dev)
+        h_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in eo.items()
+                 if k == "hist" or (k == "diff" and do_diff) or (k == "ds" and do_ds)}
         cs = torch.cuda.Stream(dev)
 
         def e2e_step():
-            hj.run(eo, ("hist", "shotdiff"), bins, stream=stream, copy_stream=cs)
-            h_hist.copy_(eo["hist"], non_blocking=True)
-            h_diff.copy_(eo["diff"], non_blocking=True)
+            hj.run(eo, ops, bins, stream=stream, copy_stream=cs)
+            for k, hv in h_out.items():
+                hv.copy_(eo[k], non_blocking=True)
 
         for _ in range(max(args.warmup, 1)):
             e2e_step()
@@ -317,7 +325,7 @@ def run_b200(args):
         e2e_ms = float(te[0]) / ksteps
         e2e = {"value": ne / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int((ee - eb) * wl.frame_bytes),
-               "d2h_bytes_per_step": int((ee - eb) * (3 * bins * 4 + 4)),
+               "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in h_out.values())),
                "positions_per_step": ne, "ms_per_step": e2e_ms,
                "path": "scn_run_pipeline_host: pinned host frames -> double-buffered H2D (copy stream) -> "
                        "hist+shotdiff kernels -> D2H of hist+diff"}
@@ -340,22 +348,25 @@ def run_b200(args):
     if rank == 0:
         peak, peak_src = load_peaks()
         F = wl.frame_bytes
-        alg_bytes = n * (F + 3 * bins * 4)  # read each sampled frame once, write 3*B u32 counts
+        ds_b = (wl.width // 2) * (wl.height // 2) * 3 if do_ds else 0
+        alg_bytes = n * (F + 3 * bins * 4 + ds_b)  # read each sampled frame once, write counts (+ ds)
         achieved = alg_bytes / (hist_ms_max / 1e3) / 1e9
-        traffic, tsrc = traffic_from_profile(n, F)
+        traffic, tsrc = traffic_from_profile(n, F, "histds" if do_ds else "hist")
         ms_per_step = total_ms_max / args.steps
         line = {
             "metric": METRIC, "value": M / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name, "frames": M, "width": wl.width, "height": wl.height, "bins": bins,
-                       "sampling": "stride 1", "ops": "hist+shotdiff" + ("+allgather" if world > 1 else ""),
+                       "sampling": str(wl.sampling[:2] if wl.sampling[0] != "range" else ("range", len(wl.sampling[1]), wl.sampling[2])),
+                       "ops": "+".join(ops) + ("+allgather" if world > 1 else ""),
                        "content": args.mode, "parallelism": f"dp{world} contiguous shards + 1-frame halo",
                        "hist_variant": "tma_pair_lane_private",
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "hist_tma_kernel<0,4> (scn_run_histogram incl. its 3 MB memset)",
+                         "kernel": ("hist_tma_kernel<2,4,16,4> (scn_run_hist_downsample incl. memset)" if do_ds else
+                                    "hist_tma_kernel<0,4,16,0> (scn_run_histogram incl. its memset)"),
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": hist_ms_max,
                          "peak_source": peak_src, "traffic_source": tsrc},
             "cpu_baseline": cpu,

@@ -246,7 +246,8 @@ class ColumnGather:
 
     def gather(self, hist, diff, n: int):
         self.hist_pad[:n].copy_(hist[:n])
-        self.diff_pad[:n].copy_(diff[:n])
+        if diff is not None:
+            self.diff_pad[:n].copy_(diff[:n])
         if self.hist_pad.is_cuda and self.dist.get_backend() == "gloo":
             # test-only path (several ranks sharing one GPU): gloo gathers host copies
             hp, dp = self.hist_pad.cpu(), self.diff_pad.cpu()
