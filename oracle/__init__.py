@@ -52,6 +52,11 @@ def lib():
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_hist_diff_frames.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                               ctypes.c_int32, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_required_rows.argtypes = [i64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, i64p, ctypes.c_int64,
+                                            i64p]
+        L.oracle_stencil_then_sample.argtypes = [ctypes.POINTER(scn_synth.SynthSpecC), ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                                                 ctypes.c_int32, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -167,3 +172,21 @@ def hist_diff_frames(frames: np.ndarray, bins: int = 16, seg_first: bool = True)
     if rc:
         raise OracleError(rc, "hist_diff_frames")
     return H[:n], D[:n]
+
+
+def required_rows(rows, offset: int, n_rows: int) -> np.ndarray:
+    """NEXT N2: exact HIST input rows for table -> HIST -> [offset,0] stencil -> Sample(rows)."""
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    return _sample(lib().oracle_required_rows, _i64p(r) if len(r) else None, len(r), offset, n_rows)
+
+
+def stencil_then_sample(spec, videos, rows, offset: int, n_rows: int, bins: int = 16) -> np.ndarray:
+    """NEXT N2 (fig:sampling-e): D'[j] = L1(H(S_j), H(clamp(S_j + offset))) over original table rows."""
+    v = np.ascontiguousarray(videos, dtype=np.int32)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros(max(len(r), 1), dtype=np.uint32)
+    rc = lib().oracle_stencil_then_sample(ctypes.byref(spec.c), _ptr(v), _ptr(r), len(r), offset, n_rows, bins,
+                                          _ptr(out))
+    if rc:
+        raise OracleError(rc, "stencil_then_sample")
+    return out[: len(r)]

@@ -247,3 +247,74 @@ int oracle_hist_diff_frames(const uint8_t* frames, int64_t n, int32_t w, int32_t
   free(seg);
   return rc;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT N2 — stencil BEFORE sampling (fig:sampling-e; "sampling after
+ * the flow operation yields a sparse set of flow fields computed from
+ * differences between original video frames"). Graph: table -> HIST ->
+ * stencil [offset, 0] -> Sample. The stencil neighbour of sampled row r is
+ * row clamp(r + offset, 0, N-1) of the ORIGINAL table (repeat-edge clamp,
+ * S:L152; reading Q6).
+ *
+ * Per-element dependency analysis ("determine the exact set of
+ * required points"): the HIST input rows required by the sampled rows S are
+ * R = { r, clamp(r + offset) : r in S }, sorted and deduplicated.
+ * ------------------------------------------------------------------------ */
+static int cmp_i64_or(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return (x > y) - (x < y);
+}
+
+static int64_t clamp_row(int64_t r, int64_t n_rows) { return r < 0 ? 0 : (r >= n_rows ? n_rows - 1 : r); }
+
+int oracle_required_rows(const int64_t* rows, int64_t m, int32_t offset, int64_t n_rows, int64_t* out, int64_t cap,
+                         int64_t* count) {
+  if (m < 0 || n_rows < 0) return OR_EINVAL;
+  int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(2 * m + 1));
+  if (!tmp) return OR_EINVAL;
+  int64_t k = 0;
+  for (int64_t j = 0; j < m; ++j) {
+    if (rows[j] < 0 || rows[j] >= n_rows) { free(tmp); return OR_ERANGE; }
+    tmp[k++] = rows[j];                              /* the sampled row itself (stencil offset 0) */
+    tmp[k++] = clamp_row(rows[j] + offset, n_rows);  /* its stencil neighbour */
+  }
+  qsort(tmp, (size_t)k, sizeof(int64_t), cmp_i64_or);
+  int64_t u = 0;
+  for (int64_t i = 0; i < k; ++i) {
+    if (i == 0 || tmp[i] != tmp[i - 1]) {
+      if (out && u < cap) out[u] = tmp[i];
+      ++u;
+    }
+  }
+  free(tmp);
+  *count = u;
+  return OR_OK;
+}
+
+/* D'[j] = sum_c sum_b |H(frame S_j)[c][b] - H(frame clamp(S_j + offset))[c][b]| for
+ * positions j of a (multi-table) sampled sequence; frames from scn_synth. */
+int oracle_stencil_then_sample(const synth_spec* spec, const int32_t* videos, const int64_t* rows, int64_t m,
+                               int32_t offset, int64_t n_rows, int32_t bins, uint32_t* diff) {
+  if (bins < 1 || bins > 256) return OR_EUNSUPPORTED;
+  const int64_t F = (int64_t)spec->width * spec->height * 3;
+  const int64_t k = 3 * (int64_t)bins;
+  uint8_t* frame = (uint8_t*)malloc((size_t)(F > 0 ? F : 1));
+  uint32_t* pair = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(2 * k));
+  if (!frame || !pair) { free(frame); free(pair); return OR_EINVAL; }
+  const uint8_t seg2[2] = {1, 0};
+  for (int64_t j = 0; j < m; ++j) {
+    const int64_t nb = clamp_row(rows[j] + offset, n_rows);
+    synth_frame_desc d = synth_describe(spec, videos[j], nb);
+    synth_fill_frame_host(spec, &d, frame);
+    oracle_hist(frame, spec->width, spec->height, bins, pair);      /* neighbour */
+    d = synth_describe(spec, videos[j], rows[j]);
+    synth_fill_frame_host(spec, &d, frame);
+    oracle_hist(frame, spec->width, spec->height, bins, pair + k);  /* sampled frame */
+    uint32_t dd[2];
+    oracle_shotdiff(pair, seg2, 2, bins, dd);
+    diff[j] = dd[1];
+  }
+  free(frame);
+  free(pair);
+  return OR_OK;
+}
