@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames-per-step", type=int, default=16)
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    ap.add_argument("--graph", default="f", choices=["f", "e"],
+                    help="f: sample -> hist -> [-1,0] (default); e: hist -> [-1,0] -> sample (NEXT N2, N = 1)")
     return ap.parse_args()
 
 
@@ -196,6 +198,48 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def run_graph_e(args):
+    """NEXT N2 (fig:sampling-e): HIST over the exact required set R = S U (S-1), then D'[j] from row pairs."""
+    import torch
+
+    import scn_harness
+    import scn_synth
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = scn_synth.WORKLOADS[args.config]
+    st = torch.cuda.current_stream(dev)
+    job = scn_harness.StencilJob(wl, -1, device=dev, stream=st, spec=wl.spec(mode=args.mode))
+    out = job.alloc_outputs()
+    for _ in range(max(args.warmup, 0)):
+        job.run(out)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    for k in range(args.steps):
+        ev[k][0].record(st)
+        launches += job.run(out)
+        ev[k][1].record(st)
+    t1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / args.steps
+    peak, peak_src = load_peaks()
+    alg = job.R * (wl.frame_bytes + 3 * wl.bins * 4)
+    line = {"metric": METRIC, "value": job.M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name + " graph e (hist -> [-1,0] -> sample)", "frames": job.M,
+                       "required_frames": job.R, "bins": wl.bins, "ops": "hist(R)+diff_pairs"},
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_step": alg},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches}
+    print(json.dumps(line), flush=True)
+    job.close()
+    return 0
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -386,6 +430,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.graph == "e":
+        return run_graph_e(args)
     return run_b200(args)
 
 

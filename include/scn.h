@@ -186,6 +186,27 @@ scn_status scn_run_pipeline_host(const scn_seq* s, int64_t begin, int64_t end, i
                                  uint32_t* d_hist, uint32_t* d_diff, uint8_t* d_out, uint32_t* d_scratch,
                                  void* d_staging, size_t staging_bytes, void* stream, void* copy_stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT N2 — stencil BEFORE sampling (fig:sampling-e; "sampling after
+ * the flow operation yields a sparse set of flow fields computed from
+ * differences between original video frames"). Graph: table -> HIST ->
+ * [offset,0] stencil -> Sample. For the sampled sequence s (rows S per part),
+ * computes the exact required HIST input set R = S U clamp(S + offset) per
+ * table (per-element dependency analysis; repeat-edge clamp to
+ * [0, N-1], reading Q6) as a new sequence `required` (per part sorted and
+ * unique, rows resolved through the table s was sampled from; the caller
+ * destroys it), and for every position j of s the positions in `required` of
+ * S_j (h_pos[j]) and of its neighbour (h_nbr[j]); both host arrays hold M.
+ * Then D'[j] = sum |H[h_pos[j]] - H[h_nbr[j]]| with scn_run_histogram over
+ * `required` and scn_run_diff_pairs.
+ * ------------------------------------------------------------------------- */
+scn_status scn_seq_stencil_required(const scn_seq* s, int32_t offset, scn_seq** required, int64_t* h_pos,
+                                    int64_t* h_nbr);
+/* d_diff[j] = sum_c sum_b |d_hist[d_a[j]][c][b] - d_hist[d_b[j]][c][b]| (u32) for j < n;
+ * d_a/d_b: device int64 row indices into d_hist ([rows][3][bins]). */
+scn_status scn_run_diff_pairs(const uint32_t* d_hist, const int64_t* d_a, const int64_t* d_b, int64_t n,
+                              int32_t bins, uint32_t* d_diff, void* stream);
+
 /* Launch statistics for the last scn_run_* call on this thread: number of
  * kernels launched and the histogram kernel variant used (for bench.py's
  * gpu_launches count). */

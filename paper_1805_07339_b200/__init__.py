@@ -67,6 +67,8 @@ _sig("scn_run_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp
 _sig("scn_run_hist_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_downsample", ctypes.c_int, _vp, _i64, _i64, _vp, _vp)
 _sig("scn_run_hist_downsample", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp)
+_sig("scn_seq_stencil_required", ctypes.c_int, _vp, _i32, _pp, _vp, _vp)
+_sig("scn_run_diff_pairs", ctypes.c_int, _vp, _vp, _vp, _i64, _i32, _vp, _vp)
 _sig("scn_run_pipeline_host", ctypes.c_int, _vp, _i64, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp)
 
 
@@ -229,6 +231,22 @@ def scn_run_pipeline_host(s, begin, end, bins, ops, d_hist, d_diff, d_out, d_scr
     _check(_lib.scn_run_pipeline_host(s, begin, end, bins, ops, _ptr(d_hist), _ptr(d_diff), _ptr(d_out),
                                       _ptr(d_scratch), _ptr(d_staging), staging_bytes, _stream(stream),
                                       _stream(copy_stream)), "scn_run_pipeline_host")
+
+
+def scn_seq_stencil_required(s, offset):
+    """NEXT N2: returns (required_seq, pos[M], nbr[M]) for table -> HIST -> [offset,0] stencil -> Sample."""
+    m = scn_seq_length(s)
+    pos = np.zeros(max(m, 1), dtype=np.int64)
+    nbr = np.zeros(max(m, 1), dtype=np.int64)
+    out = _vp()
+    _check(_lib.scn_seq_stencil_required(s, offset, ctypes.byref(out), pos.ctypes.data, nbr.ctypes.data),
+           "scn_seq_stencil_required")
+    return out, pos[:m], nbr[:m]
+
+
+def scn_run_diff_pairs(d_hist, d_a, d_b, n, bins, d_diff, stream=None) -> None:
+    _check(_lib.scn_run_diff_pairs(_ptr(d_hist), _ptr(d_a), _ptr(d_b), n, bins, _ptr(d_diff), _stream(stream)),
+           "scn_run_diff_pairs")
 
 
 __all__ = [n for n in dir() if n.startswith(("scn_", "SCN_"))] + ["ScnError", "ScnBlock", "LIB_PATH"]

@@ -475,6 +475,28 @@ __global__ void __launch_bounds__(256) shotdiff_kernel(const uint32_t* __restric
   if (lane == 0) diff[pos] = s;
 }
 
+// K3e: D[j] = sum |H[a_j] - H[b_j]| over explicit row pairs (NEXT N2, fig:sampling-e):
+// the histogram column covers the required set R; a_j / b_j index the sampled row
+// and its stencil neighbour in R.
+__global__ void __launch_bounds__(256) diff_pairs_kernel(const uint32_t* __restrict__ hist,
+                                                          const int64_t* __restrict__ ia,
+                                                          const int64_t* __restrict__ ib, int64_t n, int32_t bins,
+                                                          uint32_t* __restrict__ diff) {
+  const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pos >= n) return;
+  const int K = 3 * bins;
+  const uint32_t* x = hist + ia[pos] * K;
+  const uint32_t* y = hist + ib[pos] * K;
+  uint32_t s = 0;
+  for (int i = lane; i < K; i += 32) {
+    const uint32_t a = x[i], b = y[i];
+    s += a > b ? a - b : b - a;
+  }
+  s = __reduce_add_sync(0xFFFFFFFFu, s);
+  if (lane == 0) diff[pos] = s;
+}
+
 // ---------------------------------------------------------------------------
 // K4: downsample. Vectorised path (W % 16 == 0): one thread per 8 output pixels
 // from two 48-byte LDG.128 x3 loads; generic path: one thread per output byte.
@@ -744,4 +766,14 @@ cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, cons
   return cudaGetLastError();
 }
 
+}  // namespace scn
+
+namespace scn {
+cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int64_t* b, int64_t n, int32_t bins,
+                              uint32_t* diff, cudaStream_t st, int* launches) {
+  if (n <= 0) return cudaSuccess;
+  *launches += 1;
+  diff_pairs_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(hist, a, b, n, bins, diff);
+  return cudaGetLastError();
+}
 }  // namespace scn

@@ -32,6 +32,9 @@ cudaError_t launch_hist_downsample(const HistJob& job, cudaStream_t st, int* lau
 // histogram of the position before the first (used iff !seg[0]).
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
                             int32_t bins, uint32_t* diff, cudaStream_t st, int* launches);
+// D[j] = sum |H[a[j]] - H[b[j]]| (NEXT N2: stencil before sampling)
+cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int64_t* b, int64_t n, int32_t bins,
+                              uint32_t* diff, cudaStream_t st, int* launches);
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
                               cudaStream_t st, int* launches);
 

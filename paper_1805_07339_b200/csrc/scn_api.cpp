@@ -8,7 +8,9 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <string>
 #include <vector>
@@ -51,6 +53,7 @@ struct scn_table {
 
 struct scn_seq {
   int32_t width = 0, height = 0, where = 0;
+  std::vector<std::shared_ptr<const scn_table>> tables;  // per part: the sampled table (rows outside S, N2)
   std::vector<uint64_t> addr;  // frame address per position
   std::vector<int32_t> part;   // part index per position
   std::vector<int64_t> row;    // table row per position
@@ -131,6 +134,7 @@ static scn_status make_seq(const scn_table* t, const std::vector<int64_t>& rows,
   s->row = rows;
   s->seg.assign(m, 0);
   if (m) s->seg[0] = 1;
+  s->tables.push_back(std::make_shared<const scn_table>(*t));
   // absent sparse rows (address 0) are allowed here; a run that touches one
   // returns SCN_ERANGE (residency is checked per run, i.e. per work packet)
   for (size_t j = 0; j < m; ++j) s->addr[j] = t->addr(rows[j]);
@@ -202,6 +206,7 @@ scn_status scn_seq_concat(const scn_seq* const* parts, int32_t n, scn_seq** out)
     s->row.insert(s->row.end(), p->row.begin(), p->row.end());
     s->part.insert(s->part.end(), m, i);
     for (size_t j = 0; j < m; ++j) s->seg.push_back(j == 0 ? 1 : 0);
+    s->tables.push_back(p->tables.empty() ? nullptr : p->tables[0]);
   }
   *out = s;
   return SCN_OK;
@@ -262,6 +267,78 @@ scn_status scn_seq_upload(scn_seq* s, void* d_ws, size_t bytes, void* stream) {
 }
 
 void scn_seq_destroy(scn_seq* s) { delete s; }
+
+// ---------------------------------------------------------------------------
+// NEXT N2: stencil before sampling (fig:sampling-e) — exact required set
+// ---------------------------------------------------------------------------
+scn_status scn_seq_stencil_required(const scn_seq* s, int32_t offset, scn_seq** required, int64_t* h_pos,
+                                    int64_t* h_nbr) {
+  if (!s || !required) return fail(SCN_EINVAL, "NULL argument");
+  *required = nullptr;
+  const size_t m = s->addr.size();
+  if (m && (!h_pos || !h_nbr)) return fail(SCN_EINVAL, "h_pos/h_nbr must hold M entries");
+  scn_seq* r = new (std::nothrow) scn_seq();
+  if (!r) return fail(SCN_EINVAL, "out of host memory");
+  r->width = s->width;
+  r->height = s->height;
+  r->where = s->where;
+  size_t j0 = 0;
+  int32_t part = 0;
+  while (j0 < m) {
+    size_t j1 = j0 + 1;
+    while (j1 < m && !s->seg[j1]) ++j1;  // positions [j0, j1) are one part (one table)
+    const std::shared_ptr<const scn_table>& t = s->tables[(size_t)s->part[j0]];
+    if (!t) {
+      delete r;
+      return fail(SCN_EINVAL, "sequence part has no table");
+    }
+    // required rows of this table: S and clamp(S + offset) (repeat-edge, reading Q6), sorted, unique
+    std::vector<int64_t> rows;
+    rows.reserve(2 * (j1 - j0));
+    for (size_t j = j0; j < j1; ++j) {
+      const int64_t x = s->row[j];
+      int64_t nb = x + offset;
+      nb = nb < 0 ? 0 : (nb >= t->rows ? t->rows - 1 : nb);
+      rows.push_back(x);
+      rows.push_back(nb);
+    }
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    const int64_t base = (int64_t)r->addr.size();
+    for (size_t i = 0; i < rows.size(); ++i) {
+      r->addr.push_back(t->addr(rows[i]));
+      r->row.push_back(rows[i]);
+      r->part.push_back(part);
+      r->seg.push_back(i == 0 ? 1 : 0);
+    }
+    r->tables.push_back(t);
+    for (size_t j = j0; j < j1; ++j) {
+      const int64_t x = s->row[j];
+      int64_t nb = x + offset;
+      nb = nb < 0 ? 0 : (nb >= t->rows ? t->rows - 1 : nb);
+      h_pos[j] = base + (std::lower_bound(rows.begin(), rows.end(), x) - rows.begin());
+      h_nbr[j] = base + (std::lower_bound(rows.begin(), rows.end(), nb) - rows.begin());
+    }
+    ++part;
+    j0 = j1;
+  }
+  *required = r;
+  return SCN_OK;
+}
+
+scn_status scn_run_diff_pairs(const uint32_t* d_hist, const int64_t* d_a, const int64_t* d_b, int64_t n,
+                              int32_t bins, uint32_t* d_diff, void* stream) {
+  g_launches = 0;
+  if (n < 0) return fail(SCN_EINVAL, "n < 0");
+  if (bins < 1 || bins > 256) return fail(SCN_EUNSUPPORTED, "bins must be in [1,256], got %d", bins);
+  if (n == 0) return SCN_OK;
+  if (!d_hist || !d_a || !d_b || !d_diff) return fail(SCN_EINVAL, "NULL device buffer");
+  int nl = 0;
+  cudaError_t e = scn::launch_diff_pairs(d_hist, d_a, d_b, n, bins, d_diff, (cudaStream_t)stream, &nl);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "diff_pairs launch");
+  return SCN_OK;
+}
 
 // ---------------------------------------------------------------------------
 // runs

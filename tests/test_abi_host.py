@@ -188,3 +188,39 @@ def test_plan_matches_oracle_sampling(name):
     assert seg.sum() == wl.n_videos
     expect_m = {"C1": 240, "C2": 16384, "C3": 36864, "C4": 4096, "C5": 7168}[name]
     assert len(row) == expect_m
+
+
+def test_n2_stencil_required_matches_oracle():
+    rng = random.Random(91)
+    for _ in range(200):
+        nv = rng.randint(1, 3)
+        parts, tables, expect_rows, S_all = [], [], [], []
+        for v in range(nv):
+            n = rng.randint(1, 40)
+            t = _table(n)
+            tables.append(t)
+            rows = sorted(rng.sample(range(n), rng.randint(1, n)))
+            parts.append(scn.scn_sample_gather(t, rows))
+            S_all.append((rows, n))
+        q = scn.scn_seq_concat(parts) if nv > 1 else parts[0]
+        o = rng.randint(-4, 4)
+        req, pos, nbr = scn.scn_seq_stencil_required(q, o)
+        rpart, rrow = scn.scn_seq_rows(req)
+        seg = scn.scn_seq_seg_starts(req)
+        exp_rows, exp_part = [], []
+        for v, (rows, n) in enumerate(S_all):
+            rr = oracle.required_rows(rows, o, n).tolist()
+            exp_rows += rr
+            exp_part += [v] * len(rr)
+        assert rrow.tolist() == exp_rows and rpart.tolist() == exp_part
+        assert seg.sum() == nv
+        j = 0
+        for v, (rows, n) in enumerate(S_all):
+            for r in rows:
+                assert rrow[pos[j]] == r and rpart[pos[j]] == v
+                assert rrow[nbr[j]] == min(max(r + o, 0), n - 1) and rpart[nbr[j]] == v
+                j += 1
+        for x in [req] + ([q] if nv > 1 else []) + parts:
+            scn.scn_seq_destroy(x)
+        for t in tables:
+            scn.scn_table_destroy(t)
