@@ -57,6 +57,8 @@ def lib():
         L.oracle_stencil_then_sample.argtypes = [ctypes.POINTER(scn_synth.SynthSpecC), ctypes.c_void_p,
                                                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
                                                  ctypes.c_int32, ctypes.c_void_p]
+        L.oracle_adaptive_cuts.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                           ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -190,3 +192,14 @@ def stencil_then_sample(spec, videos, rows, offset: int, n_rows: int, bins: int 
     if rc:
         raise OracleError(rc, "stencil_then_sample")
     return out[: len(r)]
+
+
+def adaptive_cuts(diff, seg_start, warmup: int, k_num: int, k_den: int, floor: int) -> np.ndarray:
+    """NEXT N3: bounded-state adaptive cut detector with warmup W over D -> uint8 [m]."""
+    d = np.ascontiguousarray(diff, dtype=np.uint32)
+    s = np.ascontiguousarray(seg_start, dtype=np.uint8)
+    out = np.zeros(max(len(d), 1), dtype=np.uint8)
+    rc = lib().oracle_adaptive_cuts(_ptr(d), _ptr(s), len(d), warmup, k_num, k_den, floor, _ptr(out))
+    if rc:
+        raise OracleError(rc, "adaptive_cuts")
+    return out[: len(d)]

@@ -318,3 +318,33 @@ int oracle_stencil_then_sample(const synth_spec* spec, const int32_t* videos, co
   free(pair);
   return OR_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT N3 — a bounded-state operation with warmup W ("Scanner
+ * guarantees that prior to invoking an instance of a bounded state operation
+ * to generate output element i, the operation will have previously been
+ * invoked to produce at least the previous W elements"
+ * sliding_mean, S:L361-364 threshold_detector). The op is an adaptive shot
+ * detector over the shot-diff column D: its state is the window of the last
+ * W_eff = min(W, p - s0) values of D in the current table (s0 = the table's
+ * first position; slices reset state), and
+ *   cut[p] = W_eff > 0  and  D[p]*W_eff*k_den > k_num*sum(window) + floor*W_eff*k_den
+ * i.e. D[p] > (k_num/k_den)*mean(window) + floor, evaluated exactly in 64-bit.
+ * diff/seg: [m]; cut: [m] (0/1).
+ * ------------------------------------------------------------------------ */
+int oracle_adaptive_cuts(const uint32_t* diff, const uint8_t* seg_start, int64_t m, int32_t warmup, uint32_t k_num,
+                         uint32_t k_den, uint32_t floor_, uint8_t* cut) {
+  if (warmup < 1 || k_den < 1 || m < 0) return OR_EINVAL;
+  for (int64_t p = 0; p < m; ++p) {
+    int64_t s0 = p;
+    while (s0 > 0 && !seg_start[s0]) --s0;          /* first position of p's table */
+    int64_t weff = p - s0;
+    if (weff > warmup) weff = warmup;
+    uint64_t sum = 0;
+    for (int64_t i = 1; i <= weff; ++i) sum += diff[p - i];
+    uint64_t lhs = (uint64_t)diff[p] * (uint64_t)weff * k_den;
+    uint64_t rhs = (uint64_t)k_num * sum + (uint64_t)floor_ * (uint64_t)weff * k_den;
+    cut[p] = (uint8_t)(weff > 0 && lhs > rhs ? 1 : 0);
+  }
+  return OR_OK;
+}

@@ -61,3 +61,51 @@ def test_n2_planted_cuts_distinguish_e_from_f():
     _, d_f, _ = oracle.run(sp, vids, rows, seg, 0, len(rows), 16)
     assert rows[np.nonzero(d_f > tau)[0]].tolist() == [57, 132, 198]
     assert d_e[0] == 0  # row 0 clamps to itself
+
+
+# ---------------------------------------------------------------------------
+# N3 — bounded-state adaptive cut detector with warmup W
+# ---------------------------------------------------------------------------
+def test_n3_constant_stream_never_cuts():
+    # D[p] > k*mean + c is false for a constant stream when k >= 1, c >= 0
+    for w in (1, 4, 16):
+        d = np.full(50, 777, np.uint32)
+        seg = np.zeros(50, np.uint8)
+        seg[0] = 1
+        assert oracle.adaptive_cuts(d, seg, w, 3, 2, 0).sum() == 0
+
+
+def test_n3_spike_closed_form():
+    # zeros with one spike X at p: cut exactly at p iff X > floor (mean of zeros is 0);
+    # the element after the spike sees the spike in its window and does not fire
+    for w in (1, 2, 8):
+        for x, floor in ((100, 99), (100, 100), (5, 0)):
+            d = np.zeros(40, np.uint32)
+            d[20] = x
+            seg = np.zeros(40, np.uint8)
+            seg[0] = 1
+            c = oracle.adaptive_cuts(d, seg, w, 4, 1, floor)
+            assert np.nonzero(c)[0].tolist() == ([20] if x > floor else [])
+
+
+def test_n3_step_and_warmup_window():
+    # a step from a to b (b > 4a) fires once; W_eff = min(W, p - s0) and the table start resets state
+    d = np.array([10] * 10 + [100] * 10, np.uint32)
+    seg = np.zeros(20, np.uint8)
+    seg[0] = 1
+    c = oracle.adaptive_cuts(d, seg, 3, 4, 1, 0)
+    assert np.nonzero(c)[0].tolist() == [10]   # at p=11 the window mean is 40: 100 < 4*40
+    seg[10] = 1                               # a new table at 10: no window there -> no cut at 10
+    assert oracle.adaptive_cuts(d, seg, 3, 4, 1, 0).sum() == 0
+    assert oracle.adaptive_cuts(d[:1], seg[:1], 3, 1, 1, 0).tolist() == [0]  # first element: W_eff = 0
+
+
+def test_n3_planted_cuts_c1():
+    wl = scn_synth.WORKLOADS["C1"]
+    v = np.zeros(240, np.int32)
+    r = np.arange(240)
+    seg = np.zeros(240, np.uint8)
+    seg[0] = 1
+    _, D, _ = oracle.run(wl.spec(), v, r, seg, 0, 240, 16)
+    c = oracle.adaptive_cuts(D, seg, 8, 4, 1, 64 * 36 // 8)
+    assert np.nonzero(c)[0].tolist() == [57, 131, 198]

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+make -j8 all > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_next.py -m gpu -q -x > gpurun_out/pytest_next.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_next.log
+timeout 600 python bench.py --config C3 --graph e --steps 10 --warmup 3 > gpurun_out/bench_C3e.json 2> gpurun_out/bench_C3e.err; echo "C3e rc=$?"; cat gpurun_out/bench_C3e.json; tail -3 gpurun_out/bench_C3e.err
