@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames-per-step", type=int, default=16)
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    ap.add_argument("--cuts", type=int, default=0,
+                    help="NEXT N3: add the bounded-state adaptive cut detector with warmup W to the step")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
                     help="f: sample -> hist -> [-1,0] (default); e: hist -> [-1,0] -> sample (NEXT N2, N = 1)")
     return ap.parse_args()
@@ -270,8 +272,15 @@ def run_b200(args):
     n = e - b
     bins = wl.bins
     stream = torch.cuda.current_stream(dev)
-    job = scn_harness.DeviceJob(wl, b, e, with_halo=True, spec=wl.spec(mode=args.mode), device=dev, stream=stream,
+    cut_w = args.cuts
+    jb = b
+    if cut_w > 0:  # NEXT N3: the shard starts W positions early (warmup), computed and discarded
+        meta = scn_harness._build_seq(wl)
+        jb = scn.scn_seq_warmup_begin(meta, b, cut_w)
+        scn.scn_seq_destroy(meta)
+    job = scn_harness.DeviceJob(wl, jb, e, with_halo=True, spec=wl.spec(mode=args.mode), device=dev, stream=stream,
                                 plan_=plan_)
+    d_cut = torch.empty(max(n, 1), dtype=torch.uint8, device=dev) if cut_w > 0 else None
     do_diff, do_ds = "shotdiff" in wl.ops, "downsample" in wl.ops
     ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
     out = job.alloc_outputs(ops, bins)
@@ -284,17 +293,21 @@ def run_b200(args):
         if k is not None:
             ev[k][0].record(stream)
         if do_ds:  # HIST + 2x downsample in one read of each frame (reading Q12)
-            scn.scn_run_hist_downsample(job.seq, b, e, bins, out["hist"], out["ds"], stream)
+            scn.scn_run_hist_downsample(job.seq, jb, e, bins, out["hist"], out["ds"], stream)
         else:
-            scn.scn_run_histogram(job.seq, b, e, bins, out["hist"], stream)
+            scn.scn_run_histogram(job.seq, jb, e, bins, out["hist"], stream)
         launches[0] += scn.scn_last_launch_count()
         if k is not None:
             ev[k][1].record(stream)
         if do_diff:
-            scn.scn_run_shotdiff(job.seq, b, e, bins, out["hist"], out["diff"], out["scratch"], stream)
+            scn.scn_run_shotdiff(job.seq, jb, e, bins, out["hist"], out["diff"], out["scratch"], stream)
+            launches[0] += scn.scn_last_launch_count()
+        if cut_w > 0:
+            scn.scn_run_adaptive_cuts(job.seq, b, e, cut_w, out["diff"], 4, 1, wl.width * wl.height // 8, d_cut,
+                                      stream)
             launches[0] += scn.scn_last_launch_count()
         if gather is not None:
-            gather.gather(out["hist"], out.get("diff"), n)
+            gather.gather(out["hist"][b - jb:], out["diff"][b - jb:] if do_diff else None, n)
         if k is not None:
             ev[k][2].record(stream)
 
@@ -393,7 +406,7 @@ def run_b200(args):
         peak, peak_src = load_peaks()
         F = wl.frame_bytes
         ds_b = (wl.width // 2) * (wl.height // 2) * 3 if do_ds else 0
-        alg_bytes = n * (F + 3 * bins * 4 + ds_b)  # read each sampled frame once, write counts (+ ds)
+        alg_bytes = (e - jb) * (F + 3 * bins * 4 + ds_b)  # read each frame once, write counts (+ ds)
         achieved = alg_bytes / (hist_ms_max / 1e3) / 1e9
         traffic, tsrc = traffic_from_profile(n, F, "histds" if do_ds else "hist")
         ms_per_step = total_ms_max / args.steps
@@ -403,7 +416,8 @@ def run_b200(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name, "frames": M, "width": wl.width, "height": wl.height, "bins": bins,
                        "sampling": str(wl.sampling[:2] if wl.sampling[0] != "range" else ("range", len(wl.sampling[1]), wl.sampling[2])),
-                       "ops": "+".join(ops) + ("+allgather" if world > 1 else ""),
+                       "ops": "+".join(ops) + (f"+adaptive_cuts(W={cut_w})" if cut_w else "") +
+                              ("+allgather" if world > 1 else ""),
                        "content": args.mode, "parallelism": f"dp{world} contiguous shards + 1-frame halo",
                        "hist_variant": "tma_pair_lane_private",
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},

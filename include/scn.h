@@ -207,6 +207,28 @@ scn_status scn_seq_stencil_required(const scn_seq* s, int32_t offset, scn_seq** 
 scn_status scn_run_diff_pairs(const uint32_t* d_hist, const int64_t* d_a, const int64_t* d_b, int64_t n,
                               int32_t bins, uint32_t* d_diff, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT N3 — a bounded-state operation with warmup W (the op is
+ * guaranteed to have produced "at least the previous W elements"; a split at a
+ * packet boundary recomputes W warmup elements and discards them, P:L214,
+ * "treated like a stencil operation with the footprint (i-W,...,i-1,i)",
+ * P:L255). The op is an adaptive shot detector over the shot-diff column:
+ *   cut[p] = W_eff > 0 and D[p]*W_eff*k_den > k_num*sum(D[p-W_eff..p-1]) + floor*W_eff*k_den
+ * with W_eff = min(W, p - first position of p's table) (tables are slices,
+ * P:L216), evaluated exactly in 64-bit (S:L357-364 sliding_mean/threshold).
+ *
+ * scn_seq_warmup_begin returns wb = the first position whose D a shard
+ * starting at `begin` needs: max(begin - W, first position of begin's table).
+ * scn_run_adaptive_cuts: d_diff holds D for positions [wb, end) (e.g. from
+ * scn_run_hist_shotdiff over [wb, end), whose own [-1,0] halo is recomputed);
+ * d_cut (u8, [end-begin]) gets the flags for [begin, end) only — the warmup
+ * outputs are never written. EINVAL if warmup < 1 or k_den < 1.
+ * ------------------------------------------------------------------------- */
+int64_t scn_seq_warmup_begin(const scn_seq* s, int64_t begin, int32_t warmup);
+scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, int32_t warmup,
+                                 const uint32_t* d_diff, uint32_t k_num, uint32_t k_den, uint32_t floor_,
+                                 uint8_t* d_cut, void* stream);
+
 /* Launch statistics for the last scn_run_* call on this thread: number of
  * kernels launched and the histogram kernel variant used (for bench.py's
  * gpu_launches count). */

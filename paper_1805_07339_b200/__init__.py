@@ -69,6 +69,8 @@ _sig("scn_run_downsample", ctypes.c_int, _vp, _i64, _i64, _vp, _vp)
 _sig("scn_run_hist_downsample", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp)
 _sig("scn_seq_stencil_required", ctypes.c_int, _vp, _i32, _pp, _vp, _vp)
 _sig("scn_run_diff_pairs", ctypes.c_int, _vp, _vp, _vp, _i64, _i32, _vp, _vp)
+_sig("scn_seq_warmup_begin", _i64, _vp, _i64, _i32)
+_sig("scn_run_adaptive_cuts", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _u32, _u32, _u32, _vp, _vp)
 _sig("scn_run_pipeline_host", ctypes.c_int, _vp, _i64, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp)
 
 
@@ -247,6 +249,15 @@ def scn_seq_stencil_required(s, offset):
 def scn_run_diff_pairs(d_hist, d_a, d_b, n, bins, d_diff, stream=None) -> None:
     _check(_lib.scn_run_diff_pairs(_ptr(d_hist), _ptr(d_a), _ptr(d_b), n, bins, _ptr(d_diff), _stream(stream)),
            "scn_run_diff_pairs")
+
+
+def scn_seq_warmup_begin(s, begin, warmup) -> int:
+    return int(_lib.scn_seq_warmup_begin(s, begin, warmup))
+
+
+def scn_run_adaptive_cuts(s, begin, end, warmup, d_diff, k_num, k_den, floor, d_cut, stream=None) -> None:
+    _check(_lib.scn_run_adaptive_cuts(s, begin, end, warmup, _ptr(d_diff), k_num, k_den, floor, _ptr(d_cut),
+                                      _stream(stream)), "scn_run_adaptive_cuts")
 
 
 __all__ = [n for n in dir() if n.startswith(("scn_", "SCN_"))] + ["ScnError", "ScnBlock", "LIB_PATH"]

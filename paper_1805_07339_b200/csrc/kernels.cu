@@ -777,3 +777,37 @@ cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int6
   return cudaGetLastError();
 }
 }  // namespace scn
+
+namespace scn {
+// NEXT N3: adaptive shot detector, a bounded-state op with warmup W.
+// State = window of the last W_eff = min(W, q - table start) shot-diffs; the
+// shard's first W positions before q0 are warmup: read, never written.
+__global__ void __launch_bounds__(256) adaptive_cuts_kernel(const uint32_t* __restrict__ diff,
+                                                             const uint8_t* __restrict__ seg, int64_t q0, int64_t n,
+                                                             int32_t warmup, uint32_t k_num, uint32_t k_den,
+                                                             uint32_t floor_, uint8_t* __restrict__ cut) {
+  const int64_t q = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  uint64_t sum = 0;
+  int32_t weff = 0;
+  for (int32_t i = 1; i <= warmup; ++i) {
+    if (seg[q - i + 1]) break;  // the window never crosses the table's first position
+    sum += diff[q - i];
+    weff = i;
+  }
+  const uint64_t lhs = (uint64_t)diff[q] * (uint64_t)weff * k_den;
+  const uint64_t rhs = (uint64_t)k_num * sum + (uint64_t)floor_ * (uint64_t)weff * k_den;
+  cut[q - q0] = (weff > 0 && lhs > rhs) ? 1 : 0;
+}
+
+cudaError_t launch_adaptive_cuts(const uint32_t* diff, const uint8_t* seg, int64_t q0, int64_t n, int32_t warmup,
+                                 uint32_t k_num, uint32_t k_den, uint32_t floor_, uint8_t* cut, cudaStream_t st,
+                                 int* launches) {
+  const int64_t cnt = n - q0;
+  if (cnt <= 0) return cudaSuccess;
+  *launches += 1;
+  adaptive_cuts_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(diff, seg, q0, n, warmup, k_num, k_den, floor_,
+                                                                      cut);
+  return cudaGetLastError();
+}
+}  // namespace scn

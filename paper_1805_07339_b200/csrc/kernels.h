@@ -35,6 +35,11 @@ cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, cons
 // D[j] = sum |H[a[j]] - H[b[j]]| (NEXT N2: stencil before sampling)
 cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int64_t* b, int64_t n, int32_t bins,
                               uint32_t* diff, cudaStream_t st, int* launches);
+// NEXT N3: cut[q - q0] for q in [q0, n) of a window starting at the warmup begin;
+// diff/seg are indexed from the warmup begin (0).
+cudaError_t launch_adaptive_cuts(const uint32_t* diff, const uint8_t* seg, int64_t q0, int64_t n, int32_t warmup,
+                                 uint32_t k_num, uint32_t k_den, uint32_t floor_, uint8_t* cut, cudaStream_t st,
+                                 int* launches);
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
                               cudaStream_t st, int* launches);
 

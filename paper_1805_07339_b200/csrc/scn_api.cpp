@@ -340,6 +340,38 @@ scn_status scn_run_diff_pairs(const uint32_t* d_hist, const int64_t* d_a, const 
   return SCN_OK;
 }
 
+static scn_status check_run(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, bool need_bins);
+static const uint8_t* d_seg(const scn_seq* s);
+
+// ---------------------------------------------------------------------------
+// NEXT N3: bounded-state op with warmup W
+// ---------------------------------------------------------------------------
+int64_t scn_seq_warmup_begin(const scn_seq* s, int64_t begin, int32_t warmup) {
+  if (!s || begin < 0 || warmup < 0) return -1;
+  const int64_t m = (int64_t)s->seg.size();
+  if (begin >= m) return begin;
+  int64_t p = begin;
+  for (int32_t i = 0; i < warmup && p > 0 && !s->seg[(size_t)p]; ++i) --p;  // stop at the table's start
+  return p;
+}
+
+scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, int32_t warmup,
+                                 const uint32_t* d_diff, uint32_t k_num, uint32_t k_den, uint32_t floor_,
+                                 uint8_t* d_cut, void* stream) {
+  scn_status rc = check_run(s, begin, end, 1, false);
+  if (rc) return rc;
+  if (warmup < 1 || k_den < 1) return fail(SCN_EINVAL, "warmup and k_den must be >= 1");
+  if (end == begin) return SCN_OK;
+  if (!d_diff || !d_cut) return fail(SCN_EINVAL, "d_diff/d_cut is NULL");
+  const int64_t wb = scn_seq_warmup_begin(s, begin, warmup);
+  int nl = 0;
+  cudaError_t e = scn::launch_adaptive_cuts(d_diff, d_seg(s) + wb, begin - wb, end - wb, warmup, k_num, k_den,
+                                            floor_, d_cut, (cudaStream_t)stream, &nl);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "adaptive_cuts launch");
+  return SCN_OK;
+}
+
 // ---------------------------------------------------------------------------
 // runs
 // ---------------------------------------------------------------------------

@@ -224,3 +224,18 @@ def test_n2_stencil_required_matches_oracle():
             scn.scn_seq_destroy(x)
         for t in tables:
             scn.scn_table_destroy(t)
+
+
+def test_n3_warmup_begin():
+    ta, tb = _table(10), _table(7)
+    qa, qb = scn.scn_sample_stride(ta, 1), scn.scn_sample_stride(tb, 1)
+    q = scn.scn_seq_concat([qa, qb])  # tables start at positions 0 and 10
+    seg = scn.scn_seq_seg_starts(q)
+    for b in range(17):
+        for w in range(0, 6):
+            s0 = max(i for i in range(b + 1) if seg[i]) if b < 17 else b
+            assert scn.scn_seq_warmup_begin(q, b, w) == max(s0, b - w), (b, w)
+    for x in (qa, qb, q):
+        scn.scn_seq_destroy(x)
+    scn.scn_table_destroy(ta)
+    scn.scn_table_destroy(tb)

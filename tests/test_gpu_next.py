@@ -45,3 +45,35 @@ def test_n2_c1_cuts():
     assert job.row[np.nonzero(d > 64 * 36)[0]].tolist() == [57, 198]
     assert job.R == len(oracle.required_rows(job.row, -1, 240))
     job.close()
+
+
+def _n3_ref(wl, W, kn, kd, fl):
+    part, row, seg = scn_harness.plan(wl)
+    _, D, _ = oracle.run(wl.spec(), part, row, seg, 0, len(row), wl.bins)
+    return oracle.adaptive_cuts(D, seg, W, kn, kd, fl), len(row)
+
+
+@pytest.mark.parametrize("W", [1, 4, 16])
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
+def test_n3_adaptive_cuts_sharded_with_warmup(W, G):
+    import paper_1805_07339_b200 as scn
+    wl = Workload("n3", 64, 36, 3, 70, ("stride", 1), ("hist", "shotdiff"), spec_kw={"len_min": 6, "len_max": 20})
+    kn, kd, fl = 4, 1, 64 * 36 // 8
+    ref, M = _n3_ref(wl, W, kn, kd, fl)
+    pl = scn_harness.plan(wl)
+    cuts = []
+    for r in range(G):
+        b, e = scn.scn_shard_range(M, G, r)
+        meta = scn_harness._build_seq(wl)  # metadata-only sequence: where does this shard's warmup start?
+        wb = scn.scn_seq_warmup_begin(meta, b, W)
+        scn.scn_seq_destroy(meta)
+        job = scn_harness.DeviceJob(wl, wb, e, with_halo=True, plan_=pl)
+        out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
+        job.run(out, ("hist", "shotdiff"), wl.bins)
+        c = torch.empty(max(e - b, 1), dtype=torch.uint8, device="cuda")
+        scn.scn_run_adaptive_cuts(job.seq, b, e, W, out["diff"], kn, kd, fl, c)
+        torch.cuda.synchronize()
+        cuts.append(c.cpu().numpy()[: e - b])
+        job.close()
+    np.testing.assert_array_equal(np.concatenate(cuts), ref)
+    assert ref.sum() >= 3
