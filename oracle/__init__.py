@@ -59,6 +59,10 @@ def lib():
                                                  ctypes.c_int32, ctypes.c_void_p]
         L.oracle_adaptive_cuts.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
+        L.oracle_shot_starts.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, i64p,
+                                         ctypes.c_int64, i64p]
+        L.oracle_montage.argtypes = [ctypes.POINTER(scn_synth.SynthSpecC), ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -203,3 +207,23 @@ def adaptive_cuts(diff, seg_start, warmup: int, k_num: int, k_den: int, floor: i
     if rc:
         raise OracleError(rc, "adaptive_cuts")
     return out[: len(d)]
+
+
+def shot_starts(diff, seg_start, tau: int) -> np.ndarray:
+    """NEXT N1: first position of every shot = {p : seg_start[p] or D[p] > tau} (reading Q5)."""
+    d = np.ascontiguousarray(diff, dtype=np.uint32)
+    s = np.ascontiguousarray(seg_start, dtype=np.uint8)
+    return _sample(lib().oracle_shot_starts, _ptr(d), _ptr(s), len(d), tau)
+
+
+def montage(spec, videos, rows, cols: int) -> np.ndarray:
+    """NEXT N1: keyframes (video, row) downsampled 2x and tiled cols per canvas row -> uint8 canvas."""
+    v = np.ascontiguousarray(videos, dtype=np.int32)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    k = len(r)
+    oh, ow = spec.height // 2, spec.width // 2
+    canvas = np.zeros((max(-(-k // cols), 1) * oh, cols * ow, 3), dtype=np.uint8)
+    rc = lib().oracle_montage(ctypes.byref(spec.c), _ptr(v), _ptr(r), k, cols, _ptr(canvas))
+    if rc:
+        raise OracleError(rc, "montage")
+    return canvas[: (-(-k // cols)) * oh]

@@ -348,3 +348,54 @@ int oracle_adaptive_cuts(const uint32_t* diff, const uint8_t* seg_start, int64_t
   }
   return OR_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT N1 — two-job shot montage ("detect shot boundaries (via
+ * histogram differences) ... produce film summaries via montage"; P:L457:
+ * "compute color histograms on every frame ... (to detect shot boundaries),
+ * and then sparsely computed ... on a single frame per shot"; two jobs because
+ * graphs cannot filter data-dependently).
+ * Job 1 -> D. Selection (reading Q5 threshold_detector): the first
+ * position of every shot = positions p with seg_start[p] or D[p] > tau.
+ * Job 2: Gather those frames, 2x downsample (reading Q11), place tile k of the
+ * K keyframes at tile-row k / cols, tile-column k % cols of a zeroed canvas of
+ * ceil(K/cols)*(H/2) rows x cols*(W/2) pixels (RGB8 HWC).
+ * ------------------------------------------------------------------------ */
+int oracle_shot_starts(const uint32_t* diff, const uint8_t* seg_start, int64_t m, uint32_t tau, int64_t* out,
+                       int64_t cap, int64_t* count) {
+  int64_t k = 0;
+  for (int64_t p = 0; p < m; ++p) {
+    if (seg_start[p] || diff[p] > tau) {
+      if (out && k < cap) out[k] = p;
+      ++k;
+    }
+  }
+  *count = k;
+  return OR_OK;
+}
+
+int oracle_montage(const synth_spec* spec, const int32_t* videos, const int64_t* rows, int64_t k, int32_t cols,
+                   uint8_t* canvas) {
+  if (cols < 1 || k < 0) return OR_EINVAL;
+  const int32_t ow = spec->width / 2, oh = spec->height / 2;
+  const int64_t tile_rows = (k + cols - 1) / cols;
+  const int64_t pitch = (int64_t)cols * ow * 3;
+  memset(canvas, 0, (size_t)(tile_rows * oh * pitch));
+  const int64_t F = (int64_t)spec->width * spec->height * 3;
+  uint8_t* frame = (uint8_t*)malloc((size_t)(F > 0 ? F : 1));
+  uint8_t* ds = (uint8_t*)malloc((size_t)((int64_t)ow * oh * 3 + 1));
+  if (!frame || !ds) { free(frame); free(ds); return OR_EINVAL; }
+  for (int64_t i = 0; i < k; ++i) {
+    synth_frame_desc d = synth_describe(spec, videos[i], rows[i]);
+    synth_fill_frame_host(spec, &d, frame);
+    oracle_downsample(frame, spec->width, spec->height, ds);
+    const int64_t ty = i / cols, tx = i % cols;
+    for (int32_t y = 0; y < oh; ++y)
+      for (int32_t x = 0; x < ow; ++x)
+        for (int32_t c = 0; c < 3; ++c)
+          canvas[(ty * oh + y) * pitch + (tx * ow + x) * 3 + c] = ds[((int64_t)y * ow + x) * 3 + c];
+  }
+  free(frame);
+  free(ds);
+  return OR_OK;
+}

@@ -109,3 +109,46 @@ def test_n3_planted_cuts_c1():
     _, D, _ = oracle.run(wl.spec(), v, r, seg, 0, 240, 16)
     c = oracle.adaptive_cuts(D, seg, 8, 4, 1, 64 * 36 // 8)
     assert np.nonzero(c)[0].tolist() == [57, 131, 198]
+
+
+# ---------------------------------------------------------------------------
+# N1 — two-job shot montage
+# ---------------------------------------------------------------------------
+def test_n1_shot_starts_planted():
+    wl = scn_synth.WORKLOADS["C1"]
+    v, r = np.zeros(240, np.int32), np.arange(240)
+    seg = np.zeros(240, np.uint8)
+    seg[0] = 1
+    _, D, _ = oracle.run(wl.spec(), v, r, seg, 0, 240, 16)
+    assert oracle.shot_starts(D, seg, 64 * 36).tolist() == [0, 57, 131, 198]
+    seg2 = seg.copy()
+    seg2[100] = 1  # a second table starting at 100 starts a shot too
+    assert oracle.shot_starts(D, seg2, 64 * 36).tolist() == [0, 57, 100, 131, 198]
+
+
+@pytest.mark.parametrize("cols", [1, 3, 4, 7])
+def test_n1_montage_constant_shots_closed_form(cols):
+    # constant-colour shots: each tile is the shot's base colour (downsample of a constant is the
+    # constant, reading Q11); cells past the last keyframe stay zero; canvas size is closed-form
+    sp = scn_synth.Spec(32, 18, mode="constant", cuts=[5, 9, 14, 20], seed=4)
+    rows = np.array([0, 5, 9, 14, 20])
+    vids = np.zeros(5, np.int32)
+    can = oracle.montage(sp, vids, rows, cols)
+    oh, ow = 9, 16
+    assert can.shape == (-(-5 // cols) * oh, cols * ow, 3)
+    for k, row in enumerate(rows):
+        tile = can[(k // cols) * oh:(k // cols + 1) * oh, (k % cols) * ow:(k % cols + 1) * ow]
+        base = sp.frame(0, int(row))[0, 0]
+        assert (tile == base).all()
+    for k in range(5, -(-5 // cols) * cols):
+        assert (can[(k // cols) * oh:(k // cols + 1) * oh, (k % cols) * ow:(k % cols + 1) * ow] == 0).all()
+
+
+def test_n1_montage_tile_is_downsampled_keyframe():
+    sp = scn_synth.Spec(48, 20, seed=9, len_min=3, len_max=5)
+    rows = np.array([0, 4, 9, 17])
+    vids = np.array([0, 0, 1, 1], np.int32)
+    can = oracle.montage(sp, vids, rows, 3)
+    for k in range(4):
+        tile = can[(k // 3) * 10:(k // 3 + 1) * 10, (k % 3) * 24:(k % 3 + 1) * 24]
+        np.testing.assert_array_equal(tile, oracle.downsample(sp.frame(int(vids[k]), int(rows[k]))))
