@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
     ap.add_argument("--cuts", type=int, default=0,
                     help="NEXT N3: add the bounded-state adaptive cut detector with warmup W to the step")
+    ap.add_argument("--montage", type=int, default=0,
+                    help="NEXT N1: time the two-job shot montage with this many tiles per canvas row (N = 1)")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
                     help="f: sample -> hist -> [-1,0] (default); e: hist -> [-1,0] -> sample (NEXT N2, N = 1)")
     return ap.parse_args()
@@ -237,6 +239,50 @@ def run_graph_e(args):
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                          "algorithmic_bytes_per_step": alg},
             "cpu_baseline": None, "e2e": None, "gpu_launches": launches}
+    print(json.dumps(line), flush=True)
+    job.close()
+    return 0
+
+
+def run_montage(args):
+    """NEXT N1: job 1 (hist + shot-diff over the film) -> D to host -> shot starts -> job 2
+    (gather keyframes, 2x downsample into a montage canvas). Timed end to end on the stream,
+    host selection included."""
+    import torch
+
+    import scn_harness
+    import scn_synth
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = scn_synth.WORKLOADS[args.config]
+    st = torch.cuda.current_stream(dev)
+    pl = scn_harness.plan(wl)
+    M = len(pl[1]) if args.frames <= 0 else min(args.frames, len(pl[1]))
+    pl = tuple(x[:M] for x in pl)
+    job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, device=dev, stream=st, plan_=pl,
+                                spec=wl.spec(mode=args.mode))
+    out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
+    tau = wl.width * wl.height
+    for _ in range(max(args.warmup, 1)):
+        canvas, pos = scn_harness.shot_montage(job, args.montage, tau, out=out)
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        canvas, pos = scn_harness.shot_montage(job, args.montage, tau, out=out)
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    line = {"metric": METRIC, "value": M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name + " two-job shot montage (NEXT N1)", "frames": M,
+                       "keyframes": int(len(pos)), "canvas": list(canvas.shape), "cols": args.montage,
+                       "ops": "job1 hist+shotdiff -> D2H -> select -> job2 gather+downsample montage"},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+            "step_ms_min": min(ts)}
     print(json.dumps(line), flush=True)
     job.close()
     return 0
@@ -446,6 +492,8 @@ def main():
         return run_reference(args)
     if args.graph == "e":
         return run_graph_e(args)
+    if args.montage > 0:
+        return run_montage(args)
     return run_b200(args)
 
 

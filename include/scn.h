@@ -229,6 +229,31 @@ scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, i
                                  const uint32_t* d_diff, uint32_t k_num, uint32_t k_den, uint32_t floor_,
                                  uint8_t* d_cut, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT N1 — two-job shot montage ("detect shot boundaries (via
+ * histogram differences) ... produce film summaries via montage"; P:L457:
+ * histograms on every frame, then "sparsely computed ... on a single frame per
+ * shot"). A graph cannot filter data-dependently, so this is two
+ * jobs with host selection in between:
+ *   job 1: scn_run_hist_shotdiff -> D (copied to the host);
+ *   scn_select_shot_starts: positions p in [begin,end) with seg_start[p] or
+ *     h_diff[p-begin] > tau (threshold_detector, reading Q5) are
+ *     written to h_pos (up to cap); *count = how many there are;
+ *   scn_seq_gather_positions: job 2's Gather over the sequence's own positions
+ *     (strictly increasing, EINVAL; in [0,M), ERANGE) -> a new sequence
+ *     (sampling composes; a table change starts a new part);
+ *   scn_run_montage: 2x box downsample (as scn_run_downsample) of positions
+ *     [begin,end), written as tiles into d_canvas: tile k (k = j - begin) at
+ *     tile-row k / cols, tile-column k % cols; canvas_pitch = bytes between
+ *     canvas rows (>= cols*(W/2)*3, EINVAL); the call zeroes the
+ *     ceil(k/cols)*(H/2) canvas rows it covers first.
+ * ------------------------------------------------------------------------- */
+scn_status scn_select_shot_starts(const scn_seq* s, int64_t begin, int64_t end, const uint32_t* h_diff, uint32_t tau,
+                                  int64_t* h_pos, int64_t cap, int64_t* count);
+scn_status scn_seq_gather_positions(const scn_seq* s, const int64_t* h_pos, int64_t n, scn_seq** out);
+scn_status scn_run_montage(const scn_seq* s, int64_t begin, int64_t end, int32_t cols, uint8_t* d_canvas,
+                           int64_t canvas_pitch, void* stream);
+
 /* Launch statistics for the last scn_run_* call on this thread: number of
  * kernels launched and the histogram kernel variant used (for bench.py's
  * gpu_launches count). */

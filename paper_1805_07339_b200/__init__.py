@@ -71,6 +71,9 @@ _sig("scn_seq_stencil_required", ctypes.c_int, _vp, _i32, _pp, _vp, _vp)
 _sig("scn_run_diff_pairs", ctypes.c_int, _vp, _vp, _vp, _i64, _i32, _vp, _vp)
 _sig("scn_seq_warmup_begin", _i64, _vp, _i64, _i32)
 _sig("scn_run_adaptive_cuts", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _u32, _u32, _u32, _vp, _vp)
+_sig("scn_select_shot_starts", ctypes.c_int, _vp, _i64, _i64, _vp, _u32, _vp, _i64, ctypes.POINTER(_i64))
+_sig("scn_seq_gather_positions", ctypes.c_int, _vp, _vp, _i64, _pp)
+_sig("scn_run_montage", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _i64, _vp)
 _sig("scn_run_pipeline_host", ctypes.c_int, _vp, _i64, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp)
 
 
@@ -258,6 +261,31 @@ def scn_seq_warmup_begin(s, begin, warmup) -> int:
 def scn_run_adaptive_cuts(s, begin, end, warmup, d_diff, k_num, k_den, floor, d_cut, stream=None) -> None:
     _check(_lib.scn_run_adaptive_cuts(s, begin, end, warmup, _ptr(d_diff), k_num, k_den, floor, _ptr(d_cut),
                                       _stream(stream)), "scn_run_adaptive_cuts")
+
+
+def scn_select_shot_starts(s, begin, end, h_diff, tau) -> np.ndarray:
+    """NEXT N1: positions in [begin,end) that start a shot (segment start or D > tau)."""
+    d = np.ascontiguousarray(h_diff, dtype=np.uint32)
+    cnt = _i64()
+    _check(_lib.scn_select_shot_starts(s, begin, end, d.ctypes.data, tau, None, 0, ctypes.byref(cnt)),
+           "scn_select_shot_starts")
+    out = np.zeros(max(cnt.value, 1), dtype=np.int64)
+    _check(_lib.scn_select_shot_starts(s, begin, end, d.ctypes.data, tau, out.ctypes.data, cnt.value,
+                                       ctypes.byref(cnt)), "scn_select_shot_starts")
+    return out[: cnt.value]
+
+
+def scn_seq_gather_positions(s, positions):
+    p = np.ascontiguousarray(positions, dtype=np.int64)
+    out = _vp()
+    _check(_lib.scn_seq_gather_positions(s, p.ctypes.data if len(p) else None, len(p), ctypes.byref(out)),
+           "scn_seq_gather_positions")
+    return out
+
+
+def scn_run_montage(s, begin, end, cols, d_canvas, canvas_pitch, stream=None) -> None:
+    _check(_lib.scn_run_montage(s, begin, end, cols, _ptr(d_canvas), canvas_pitch, _stream(stream)),
+           "scn_run_montage")
 
 
 __all__ = [n for n in dir() if n.startswith(("scn_", "SCN_"))] + ["ScnError", "ScnBlock", "LIB_PATH"]

@@ -54,6 +54,8 @@ struct HistParams {
   uint32_t* out;
   uint32_t* halo_out;
   uint8_t* ds_out;
+  int64_t ds_pitch;  // bytes between output rows
+  int32_t ds_cols;   // > 0: montage tiles (NEXT N1)
   int64_t F;
   int32_t width, height, bins;
   uint32_t tile;          // bytes per full tile
@@ -67,6 +69,14 @@ struct HistParams {
 
 __device__ __forceinline__ uint64_t frame_addr(const FrameSrc& s, int64_t i) {
   return s.ptrs ? s.ptrs[i] : s.base + (uint64_t)i * s.stride;
+}
+
+// First output byte of downsampled frame io: contiguous frames (cols == 0) or
+// tile (io / cols, io % cols) of a montage canvas with row pitch `pitch` (NEXT N1).
+__device__ __forceinline__ uint8_t* ds_frame_base(uint8_t* base, int64_t io, int64_t oh, int64_t ow3, int64_t pitch,
+                                                  int32_t cols) {
+  if (cols > 0) return base + (io / cols) * oh * pitch + (io % cols) * ow3;
+  return base + io * oh * pitch;
 }
 
 struct Layout {
@@ -378,9 +388,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       const uint32_t rows = len / rowb;
       const uint32_t npairs = (rows / 2) * upr;
       const int64_t ow3 = (int64_t)(p.width / 2) * 3;
+      const int64_t pitch = p.ds_pitch;
       uint8_t* dsf = (item >= p.n_halo)
-                         ? p.ds_out + (item - p.n_halo) * ((int64_t)(p.height / 2) * ow3) +
-                               ((int64_t)k * (p.rows_per_tile / 2)) * ow3
+                         ? ds_frame_base(p.ds_out, item - p.n_halo, p.height / 2, ow3, pitch, p.ds_cols) +
+                               ((int64_t)k * (p.rows_per_tile / 2)) * pitch
                          : nullptr;
       for (uint32_t u = first; u < npairs; u += kConsThreads) {
         const uint32_t rp = u / upr, xc = u - rp * upr;
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
         if (dsf) {
           ds_unit_v<(VAR >> 2) & 1>(wt, wb, o);
-          st_global_24(dsf + (int64_t)rp * ow3 + xc * 24, o);
+          st_global_24(dsf + (int64_t)rp * pitch + xc * 24, o);
         }
       }
       if (MODE == 2 && (rows & 1)) {  // odd last row of an odd-height frame: histogram only
@@ -511,13 +522,14 @@ __device__ __forceinline__ void ldg_unit(const uint8_t* p, uint32_t* w) {
 
 // one block per (output row y = blockIdx.x, frame = item0 + blockIdx.y); threads over 48-byte column units
 __global__ void __launch_bounds__(128) downsample_vec_kernel(FrameSrc src, int64_t item0, int32_t width,
-                                                             int32_t height, uint8_t* __restrict__ out) {
+                                                             int32_t height, uint8_t* __restrict__ out,
+                                                             int64_t pitch, int32_t cols) {
   const uint32_t upr = (uint32_t)width / 16u, oh = (uint32_t)height / 2u;
   const uint32_t y = blockIdx.x;
   const int64_t item = item0 + blockIdx.y;
   const uint32_t rowb = (uint32_t)width * 3u, ow3 = (uint32_t)(width / 2) * 3u;
   const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item)) + (size_t)(2u * y) * rowb;
-  uint8_t* o = out + item * ((int64_t)oh * ow3) + (int64_t)y * ow3;
+  uint8_t* o = ds_frame_base(out, item, oh, ow3, pitch, cols) + (int64_t)y * pitch;
   for (uint32_t xc = threadIdx.x; xc < upr; xc += blockDim.x) {
     uint32_t wt[12], wb[12], r[6];
     ldg_unit(f + xc * 48u, wt);
@@ -528,7 +540,8 @@ __global__ void __launch_bounds__(128) downsample_vec_kernel(FrameSrc src, int64
 }
 
 __global__ void __launch_bounds__(256) downsample_generic_kernel(FrameSrc src, int64_t n, int32_t width,
-                                                                 int32_t height, uint8_t* __restrict__ out) {
+                                                                 int32_t height, uint8_t* __restrict__ out,
+                                                                 int64_t pitch, int32_t cols) {
   const int32_t ow = width / 2, oh = height / 2;
   const int64_t per = (int64_t)ow * oh * 3;
   const int64_t total = per * n;
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(256) downsample_generic_kernel(FrameSrc src, i
     const uint8_t* f = reinterpret_cast<const uint8_t*>(frame_addr(src, item));
     const int64_t i00 = ((2 * y) * width + 2 * x) * 3 + c;
     const uint32_t s = (uint32_t)f[i00] + f[i00 + 3] + f[i00 + (int64_t)width * 3] + f[i00 + (int64_t)width * 3 + 3];
-    out[g] = (uint8_t)((s + 2u) >> 2);
+    ds_frame_base(out, item, oh, (int64_t)ow * 3, pitch, cols)[y * pitch + x * 3 + c] = (uint8_t)((s + 2u) >> 2);
   }
 }
 
@@ -622,6 +635,8 @@ static HistParams base_params(const HistJob& j) {
   p.out = j.out;
   p.halo_out = j.halo_out;
   p.ds_out = j.ds_out;
+  p.ds_pitch = j.ds_pitch > 0 ? j.ds_pitch : (int64_t)(j.width / 2) * 3;
+  p.ds_cols = j.ds_cols;
   p.F = (int64_t)j.width * j.height * 3;
   p.width = j.width;
   p.height = j.height;
@@ -667,30 +682,31 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
 }
 
 static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int64_t pitch, int32_t cols);
 
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
-                              cudaStream_t st, int* launches) {
+                              cudaStream_t st, int* launches, int64_t ds_pitch, int32_t ds_cols, bool allow_vec) {
+  const int64_t pitch = ds_pitch > 0 ? ds_pitch : (int64_t)(width / 2) * 3;
   cudaError_t e = device_props();
   if (e != cudaSuccess) return e;
   if (n <= 0 || width < 2 || height < 2) return cudaSuccess;
   read_tuning();
-  if (width % 16 == 0 && g_ds_impl == 0 && (int64_t)width * 6 <= 65536) {
+  if (allow_vec && width % 16 == 0 && g_ds_impl == 0 && (int64_t)width * 6 <= 65536) {
     *launches += 1;
-    return launch_ds_tma(src, n, width, height, out, st);
+    return launch_ds_tma(src, n, width, height, out, st, pitch, ds_cols);
   }
-  if (width % 16 == 0) {
+  if (allow_vec && width % 16 == 0) {
     *launches += (int)((n + 65534) / 65535);
     const int threads = width / 16 >= 128 ? 128 : ((width / 16 + 31) / 32) * 32;
     for (int64_t i0 = 0; i0 < n; i0 += 65535) {
       const int64_t cnt = n - i0 < 65535 ? n - i0 : 65535;
       dim3 grid((unsigned)(height / 2), (unsigned)cnt);
-      downsample_vec_kernel<<<grid, threads, 0, st>>>(src, i0, width, height, out);
+      downsample_vec_kernel<<<grid, threads, 0, st>>>(src, i0, width, height, out, pitch, ds_cols);
     }
   } else {
     *launches += 1;
     const int grid = g_num_sms * 8;
-    downsample_generic_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out);
+    downsample_generic_kernel<<<grid, 256, 0, st>>>(src, n, width, height, out, pitch, ds_cols);
   }
   return cudaGetLastError();
 }
@@ -711,7 +727,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     e = launch_histogram(h, st, launches);
     if (e != cudaSuccess) return e;
     FrameSrc src = j.src;
-    return launch_downsample(src, j.n_items, j.width, j.height, j.ds_out, st, launches);
+    return launch_downsample(src, j.n_items, j.width, j.height, j.ds_out, st, launches, j.ds_pitch, j.ds_cols);
   }
   HistParams p = base_params(j);
   p.rows_per_tile = rpt;
@@ -735,8 +751,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
 
 // downsample-only TMA ring (MODE 3): same row-pair tiles, no table
 static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int64_t pitch, int32_t cols) {
   HistJob j{};
+  j.ds_pitch = pitch;
+  j.ds_cols = cols;
   j.src = src;
   j.n_items = n;
   j.ds_out = out;

@@ -21,6 +21,8 @@ struct HistJob {
   uint32_t* halo_out;  // [n_halo][3][bins]
   uint8_t* ds_out;     // fused downsample output [n_items - n_halo][H/2][W/2][3] or nullptr
   int32_t width, height, bins;
+  int64_t ds_pitch;    // bytes between output rows (0: (W/2)*3, contiguous frames)
+  int32_t ds_cols;     // > 0: montage, frame i is tile (i / cols, i % cols) of a canvas (NEXT N1)
 };
 
 // Histogram (zeroes nothing: the caller memsets out/halo_out first).
@@ -41,7 +43,8 @@ cudaError_t launch_adaptive_cuts(const uint32_t* diff, const uint8_t* seg, int64
                                  uint32_t k_num, uint32_t k_den, uint32_t floor_, uint8_t* cut, cudaStream_t st,
                                  int* launches);
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
-                              cudaStream_t st, int* launches);
+                              cudaStream_t st, int* launches, int64_t ds_pitch = 0, int32_t ds_cols = 0,
+                              bool allow_vec = true);
 
 // Variant names for reporting
 const char* hist_variant_name(int32_t bins);

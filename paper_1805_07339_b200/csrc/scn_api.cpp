@@ -373,6 +373,61 @@ scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, i
 }
 
 // ---------------------------------------------------------------------------
+// NEXT N1: two-job shot montage (two jobs because graphs cannot
+// filter data-dependently)
+// ---------------------------------------------------------------------------
+scn_status scn_select_shot_starts(const scn_seq* s, int64_t begin, int64_t end, const uint32_t* h_diff, uint32_t tau,
+                                  int64_t* h_pos, int64_t cap, int64_t* count) {
+  if (!s || !count) return fail(SCN_EINVAL, "NULL argument");
+  if (begin < 0 || begin > end) return fail(SCN_EINVAL, "bad range");
+  if (end > (int64_t)s->seg.size()) return fail(SCN_ERANGE, "end > sequence length");
+  if (end > begin && !h_diff) return fail(SCN_EINVAL, "h_diff is NULL");
+  int64_t k = 0;
+  for (int64_t p = begin; p < end; ++p) {
+    if (s->seg[(size_t)p] || h_diff[p - begin] > tau) {  // threshold_detector (reading Q5)
+      if (h_pos && k < cap) h_pos[k] = p;
+      ++k;
+    }
+  }
+  *count = k;
+  return SCN_OK;
+}
+
+scn_status scn_seq_gather_positions(const scn_seq* s, const int64_t* h_pos, int64_t n, scn_seq** out) {
+  if (!s || !out || (n > 0 && !h_pos)) return fail(SCN_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (n < 0) return fail(SCN_EINVAL, "n < 0");
+  const int64_t m = (int64_t)s->addr.size();
+  for (int64_t i = 0; i < n; ++i) {
+    if (i > 0 && h_pos[i] <= h_pos[i - 1]) return fail(SCN_EINVAL, "positions must be strictly increasing");
+    if (h_pos[i] < 0 || h_pos[i] >= m) return fail(SCN_ERANGE, "position %lld outside [0,%lld)", (long long)h_pos[i],
+                                                    (long long)m);
+  }
+  scn_seq* r = new (std::nothrow) scn_seq();
+  if (!r) return fail(SCN_EINVAL, "out of host memory");
+  r->width = s->width;
+  r->height = s->height;
+  r->where = s->where;
+  int32_t last_part = -1, np = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t p = (size_t)h_pos[i];
+    if (s->part[p] != last_part) {  // a new table starts a new part (slice)
+      last_part = s->part[p];
+      ++np;
+      r->tables.push_back(s->tables.empty() ? nullptr : s->tables[(size_t)last_part]);
+      r->seg.push_back(1);
+    } else {
+      r->seg.push_back(0);
+    }
+    r->addr.push_back(s->addr[p]);
+    r->row.push_back(s->row[p]);
+    r->part.push_back(np);
+  }
+  *out = r;
+  return SCN_OK;
+}
+
+// ---------------------------------------------------------------------------
 // runs
 // ---------------------------------------------------------------------------
 static scn_status check_run(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, bool need_bins) {
@@ -486,6 +541,30 @@ scn_status scn_run_downsample(const scn_seq* s, int64_t begin, int64_t end, uint
   cudaError_t e = scn::launch_downsample(src, end - begin, s->width, s->height, d_out, (cudaStream_t)stream, &nl);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "downsample launch");
+  return SCN_OK;
+}
+
+scn_status scn_run_montage(const scn_seq* s, int64_t begin, int64_t end, int32_t cols, uint8_t* d_canvas,
+                           int64_t canvas_pitch, void* stream) {
+  scn_status rc = check_run(s, begin, end, 0, false);
+  if (rc) return rc;
+  if (cols < 1) return fail(SCN_EINVAL, "cols must be >= 1");
+  const int64_t ow3 = (int64_t)(s->width / 2) * 3, oh = s->height / 2;
+  if (canvas_pitch < cols * ow3) return fail(SCN_EINVAL, "canvas pitch %lld < cols*(W/2)*3", (long long)canvas_pitch);
+  if (end == begin || oh == 0 || ow3 == 0) return SCN_OK;
+  if (!d_canvas) return fail(SCN_EINVAL, "d_canvas is NULL");
+  if ((rc = check_resident(s, begin, end))) return rc;
+  const int64_t k = end - begin, tile_rows = (k + cols - 1) / cols;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(d_canvas, 0, (size_t)(tile_rows * oh * canvas_pitch), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(canvas)");
+  // 8-byte vector stores need 8-aligned tiles; other layouts take the bytewise kernel
+  const bool aligned = ((uintptr_t)d_canvas % 8 == 0) && canvas_pitch % 8 == 0 && ow3 % 8 == 0;
+  scn::FrameSrc src{d_addr(s) + begin, 0, 0};
+  int nl = 0;
+  e = scn::launch_downsample(src, k, s->width, s->height, d_canvas, st, &nl, canvas_pitch, cols, aligned);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "montage launch");
   return SCN_OK;
 }
 

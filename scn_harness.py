@@ -336,3 +336,33 @@ class StencilJob:
             self.close()
         except Exception:
             pass
+
+
+def shot_montage(job: "DeviceJob", cols: int, tau: int, out=None, stream=None):
+    """NEXT N1: the two-job film summary over a DeviceJob's positions [p0, p1).
+
+    Job 1: HIST + shot-diff; the D column goes to the host, where the first position of
+    every shot is selected (D > tau or a table start, reading Q5); job 2: Gather those
+    positions and write their 2x downsample as montage tiles. Returns (canvas, positions)."""
+    wl = job.wl
+    st = stream if stream is not None else job.stream
+    if out is None:
+        out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
+    b, e = job.p0, job.p1
+    scn.scn_run_hist_shotdiff(job.seq, b, e, wl.bins, out["hist"], out["diff"], out["scratch"], st)
+    d = torch.empty(max(e - b, 1), dtype=torch.int32, pin_memory=True)
+    d.copy_(out["diff"][: max(e - b, 1)], non_blocking=True)
+    st.synchronize()
+    pos = scn.scn_select_shot_starts(job.seq, b, e, d.numpy().view(np.uint32)[: e - b], tau)
+    kseq = scn.scn_seq_gather_positions(job.seq, pos)
+    try:
+        k = len(pos)
+        ws = torch.empty(max(scn.scn_seq_device_bytes(kseq), 16), dtype=torch.uint8, device=job.device)
+        scn.scn_seq_upload(kseq, ws, ws.numel(), st)
+        oh, ow = wl.height // 2, wl.width // 2
+        canvas = torch.empty((max(-(-k // cols), 1) * oh, cols * ow, 3), dtype=torch.uint8, device=job.device)
+        scn.scn_run_montage(kseq, 0, k, cols, canvas, cols * ow * 3, st)
+        st.synchronize()
+    finally:
+        scn.scn_seq_destroy(kseq)
+    return canvas[: (-(-k // cols)) * oh], pos

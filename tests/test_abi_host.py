@@ -239,3 +239,38 @@ def test_n3_warmup_begin():
         scn.scn_seq_destroy(x)
     scn.scn_table_destroy(ta)
     scn.scn_table_destroy(tb)
+
+
+def test_n1_select_and_gather_positions_match_oracle():
+    rng = np.random.default_rng(8)
+    ta, tb = _table(30), _table(25)
+    qa, qb = scn.scn_sample_stride(ta, 2), scn.scn_sample_stride(tb, 3)
+    q = scn.scn_seq_concat([qa, qb])
+    m = scn.scn_seq_length(q)
+    seg = scn.scn_seq_seg_starts(q)
+    part, row = scn.scn_seq_rows(q)
+    for _ in range(50):
+        d = rng.integers(0, 100, m).astype(np.uint32)
+        tau = int(rng.integers(0, 100))
+        b = int(rng.integers(0, m))
+        e = int(rng.integers(b, m + 1))
+        got = scn.scn_select_shot_starts(q, b, e, d[b:e], tau)
+        ref = oracle.shot_starts(d, seg, tau)
+        assert got.tolist() == [p for p in ref.tolist() if b <= p < e]
+        g = scn.scn_seq_gather_positions(q, got)
+        gp, gr = scn.scn_seq_rows(g)
+        gs = scn.scn_seq_seg_starts(g)
+        assert gr.tolist() == row[got].tolist()
+        # parts renumbered in order; a new part starts wherever the table changes
+        assert gs.tolist() == [1 if (i == 0 or part[got[i]] != part[got[i - 1]]) else 0 for i in range(len(got))]
+        scn.scn_seq_destroy(g)
+    with pytest.raises(scn.ScnError) as ex:
+        scn.scn_seq_gather_positions(q, [3, 3])
+    assert ex.value.status == scn.SCN_EINVAL
+    with pytest.raises(scn.ScnError) as ex:
+        scn.scn_seq_gather_positions(q, [m])
+    assert ex.value.status == scn.SCN_ERANGE
+    for x in (qa, qb, q):
+        scn.scn_seq_destroy(x)
+    scn.scn_table_destroy(ta)
+    scn.scn_table_destroy(tb)

@@ -77,3 +77,31 @@ def test_n3_adaptive_cuts_sharded_with_warmup(W, G):
         job.close()
     np.testing.assert_array_equal(np.concatenate(cuts), ref)
     assert ref.sum() >= 3
+
+
+@pytest.mark.parametrize("w,h,nv,cols", [(64, 36, 1, 2), (40, 22, 2, 3), (96, 54, 3, 5), (100, 31, 1, 4)])
+def test_n1_shot_montage(w, h, nv, cols):
+    wl = Workload("n1", w, h, nv, 150, ("stride", 1), ("hist", "shotdiff"), spec_kw={"len_min": 20, "len_max": 60})
+    pl = scn_harness.plan(wl)
+    part, row, seg = pl
+    job = scn_harness.DeviceJob(wl, 0, len(row), with_halo=True, plan_=pl)
+    canvas, pos = scn_harness.shot_montage(job, cols, w * h)
+    _, D, _ = oracle.run(wl.spec(), part, row, seg, 0, len(row), wl.bins)
+    ref_pos = oracle.shot_starts(D, seg, w * h)
+    assert pos.tolist() == ref_pos.tolist()
+    ref = oracle.montage(wl.spec(), part[ref_pos], row[ref_pos], cols)
+    np.testing.assert_array_equal(canvas.cpu().numpy(), ref)
+    job.close()
+
+
+def test_n1_montage_c2_prefix():
+    wl = scn_synth.WORKLOADS["C2"]
+    pl = scn_harness.plan(wl)
+    part, row, seg = (x[:1200] for x in pl)
+    job = scn_harness.DeviceJob(wl, 0, 1200, with_halo=True, plan_=(part, row, seg))
+    canvas, pos = scn_harness.shot_montage(job, 4, wl.width * wl.height)
+    cuts = set(wl.spec().cut_rows(0, 1200).tolist())
+    assert pos.tolist() == [0] + sorted(cuts)
+    ref = oracle.montage(wl.spec(), part[pos], row[pos], 4)
+    np.testing.assert_array_equal(canvas.cpu().numpy(), ref)
+    job.close()
