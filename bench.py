@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
     ap.add_argument("--cuts", type=int, default=0,
                     help="NEXT N3: add the bounded-state adaptive cut detector with warmup W to the step")
+    ap.add_argument("--bins", type=int, default=0, help="override the config's bins per channel (NEXT N4: 256)")
     ap.add_argument("--montage", type=int, default=0,
                     help="NEXT N1: time the two-job shot montage with this many tiles per canvas row (N = 1)")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
@@ -311,6 +312,9 @@ def run_b200(args):
             dist.init_process_group(args.dist_backend)
 
     wl = scn_synth.WORKLOADS[args.config]
+    if args.bins:
+        import dataclasses
+        wl = dataclasses.replace(wl, bins=args.bins)
     plan_ = scn_harness.plan(wl)
     M = len(plan_[1]) if args.frames <= 0 else min(args.frames, len(plan_[1]))
     plan_ = (plan_[0][:M], plan_[1][:M], plan_[2][:M])
@@ -465,7 +469,9 @@ def run_b200(args):
                        "ops": "+".join(ops) + (f"+adaptive_cuts(W={cut_w})" if cut_w else "") +
                               ("+allgather" if world > 1 else ""),
                        "content": args.mode, "parallelism": f"dp{world} contiguous shards + 1-frame halo",
-                       "hist_variant": "tma_pair_lane_private",
+                       "hist_variant": ("tma_pair_lane_private" if bins in (1, 2, 4, 8, 16) else
+                                        "tma_single_shift_lane_private" if bins in (32, 64, 128, 256) else
+                                        "tma_single_lane_private"),
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -160,6 +160,25 @@ __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4
   pair_unit_all<LOGB, VAR & 1>(w, lane4, std::make_integer_sequence<int, 24>{});
 }
 
+// Single-key lane-private counting for B = 2^LOGB in [32, 256] (NEXT N4): byte J of
+// channel J % 3 -> tab[c][bin][lane], bin = top LOGB bits; table 32 KB-aligned per
+// channel for B = 256 so the address is table | bin << 7 | lane << 2 (one LOP3).
+template <int LOGB, int J>
+__device__ __forceinline__ void single_unit_step(const uint32_t* w, uint32_t lane4) {
+  constexpr int c = J % 3;
+  constexpr int B = 1 << LOGB;
+  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<J, 7, LOGB>(w), lane4);
+  red_shared_add_off<c * B * 128>(addr);
+}
+template <int LOGB, int... J>
+__device__ __forceinline__ void single_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, J...>) {
+  (single_unit_step<LOGB, J>(w, lane4), ...);
+}
+template <int LOGB>
+__device__ __forceinline__ void hist_unit_single(const uint32_t* w, uint32_t lane4) {
+  single_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 48>{});
+}
+
 __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {
   const uint4 v0 = lds128(a), v1 = lds128(a + 16), v2 = lds128(a + 32);
   w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
@@ -283,6 +302,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   const int B = (MODE == 1) ? p.bins : BP;
+  constexpr bool kSingle = (MODE == 1 || MODE == 4);  // one key per byte: flush rows are (c, bin) directly
 
   if (threadIdx.x == 0) {
     if (L.stages < 2) __trap();
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     if constexpr (MODE == 3) return;
     named_bar(kBarId, kConsThreads);
     uint32_t* orow = out_row(item);
-    const int rows = (MODE == 1) ? 3 * B : 3 * BP * BP;
+    const int rows = kSingle ? 3 * B : 3 * BP * BP;
     for (int r = ctid; r < rows; r += kConsThreads) {
       const uint32_t ra = L.table + (uint32_t)r * 128u;
       uint32_t sum = 0;
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         sts128(a, make_uint4(0, 0, 0, 0));
       }
       if (sum) {
-        if (MODE == 1) {
+        if (kSingle) {
           red_global_add(orow + r, sum);
         } else {
           const int c = r / (BP * BP), key = r % (BP * BP);
@@ -357,7 +377,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
       }
     }
-    if (MODE != 1) {
+    if (!kSingle) {
       named_bar(kBarId, kConsThreads);
       if (ctid < 3 * BP) {
         const uint32_t v = hsum[ctid];
@@ -434,6 +454,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == 0) {
           hist_unit_pair<LOGB, VAR>(w, lane4);
+        } else if constexpr (MODE == 4) {
+          hist_unit_single<LOGB>(w, lane4);
         } else {
           const uint32_t Bu = (uint32_t)B;
 #pragma unroll
@@ -581,7 +603,9 @@ static int log2_exact(int b) {
 }
 
 const char* hist_variant_name(int32_t bins) {
-  return log2_exact(bins) >= 0 ? "tma_pair_lane_private" : "tma_single_lane_private";
+  if (log2_exact(bins) >= 0) return "tma_pair_lane_private";
+  if (bins >= 32 && (bins & (bins - 1)) == 0) return "tma_single_shift_lane_private";
+  return "tma_single_lane_private";
 }
 
 template <int MODE, int LOGB, int NW = kDefaultConsWarps, int VAR = 0>
@@ -674,6 +698,16 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
         if (g_tune_var == 2) return launch_tma<0, 4, 16, 2>(p, st);
         if (g_tune_var == 3) return launch_tma<0, 4, 16, 3>(p, st);
         return launch_tma<0, 4>(p, st);
+    }
+  }
+  if (j.bins >= 32 && (j.bins & (j.bins - 1)) == 0) {  // NEXT N4: B = 32..256, one shifted key per byte
+    p.table_bytes = 3u * (uint32_t)j.bins * 128u;
+    p.table_align = (uint32_t)j.bins * 128u;
+    switch (j.bins) {
+      case 32: return launch_tma<4, 5>(p, st);
+      case 64: return launch_tma<4, 6>(p, st);
+      case 128: return launch_tma<4, 7>(p, st);
+      default: return launch_tma<4, 8>(p, st);
     }
   }
   p.table_bytes = 3u * (uint32_t)j.bins * 128u;
