@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const uint32_t slot = L.slot(s);
     const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
-    if constexpr (MODE >= 2) {
+    if constexpr (MODE == 2 || MODE == 3) {
       // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs
       const uint32_t rowb = (uint32_t)p.width * 3u;
       const uint32_t upr = (uint32_t)p.width / 16u;
@@ -636,7 +636,8 @@ static uint32_t g_tune_tile = 0;
 static uint32_t g_fused_tile = 0;
 static int g_tune_var = 0;  // SCN_HIST_VAR: 1 = mul.hi shifts, 2 = two units/iteration, 3 = both
 static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
-static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
+static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
+static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -649,6 +650,7 @@ static void read_tuning() {
   g_tune_var = env_int("SCN_HIST_VAR", 0);
   g_ds_var = env_int("SCN_DS_VAR", 1);
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
+  g_hist_single = env_int("SCN_HIST_SINGLE", 0);
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -692,6 +694,11 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       case 2: return launch_tma<0, 2>(p, st);
       case 3: return launch_tma<0, 3>(p, st);
       default:
+        if (g_hist_single) {  // single shifted key per byte, 6 KB table (SCN_HIST_SINGLE=1)
+          p.table_bytes = 3u * 16u * 128u;
+          p.table_align = 16u * 128u;
+          return launch_tma<4, 4>(p, st);
+        }
         if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
         if (g_tune_warps == 24) return launch_tma<0, 4, 24>(p, st);
         if (g_tune_var == 1) return launch_tma<0, 4, 16, 1>(p, st);

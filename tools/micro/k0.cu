@@ -60,6 +60,36 @@ __global__ void k_atoms(uint32_t* out, long long* cycles, int iters) {
   atomicAdd(out, s);
 }
 
+// Same, without the serial LCG: 16 independent addresses per thread precomputed in registers, so the
+// loop is ATOMS-issue bound (the LCG version above is bound by its dependent IMAD chain).
+template <int MODE>
+__global__ void k_atoms_ilp(uint32_t* out, long long* cycles, int iters) {
+  extern __shared__ uint32_t tab[];
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 768 * 32; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  uint32_t a[16];
+  uint32_t x = threadIdx.x * 2654435761u + blockIdx.x * 97u + 12345u;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    x = x * 1664525u + 1013904223u;
+    uint32_t key = MODE == 0 ? ((x >> 20) % 768u) : (MODE == 1 ? (uint32_t)(u % 16) : ((x >> 20) % 48u));
+    a[u] = smem_u32(tab + key * 32 + lane);
+  }
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a[u]), "r"(1u) : "memory");
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  uint32_t s = 0;
+  for (int i = threadIdx.x; i < 768 * 32; i += blockDim.x) s += tab[i];
+  atomicAdd(out, s);
+}
+
 // ---------------- match_any / reduce_add ----------------
 template <int MODE>
 __global__ void k_warp(uint32_t* out, long long* cycles, int iters) {
@@ -211,6 +241,22 @@ int main(int argc, char** argv) {
       double lane_ops = (double)threads * iters * 16;
       printf("\"%s_t%d\": {\"lane_ops_per_clk_per_sm\": %.3f, \"ms\": %.4f, \"clk_mhz_implied\": %.0f},\n", names[mode], threads,
              lane_ops / cyc, ms, cyc / (ms * 1e3));
+    }
+  }
+  // ---- shared atomics, independent addresses (no dependent chain)
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int threads : {512, 1024}) {
+      int iters = 512;
+      size_t smem = 768 * 32 * 4;
+      void (*fn)(uint32_t*, long long*, int) = mode == 0 ? k_atoms_ilp<0> : (mode == 1 ? k_atoms_ilp<1> : k_atoms_ilp<2>);
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fn<<<nsm, threads, smem>>>(dout, dcyc, 8); CK(cudaDeviceSynchronize());
+      fn<<<nsm, threads, smem>>>(dout, dcyc, iters); CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(hc.data(), dcyc, sizeof(long long) * nsm, cudaMemcpyDeviceToHost));
+      std::vector<long long> v(hc.begin(), hc.begin() + nsm);
+      double cyc = median_cycles(v);
+      const char* nm = mode == 0 ? "atoms_ilp_lane_private_768keys" : (mode == 1 ? "atoms_ilp_lane_private_16keys_repeat" : "atoms_ilp_lane_private_48keys");
+      printf("\"%s_t%d\": {\"lane_ops_per_clk_per_sm\": %.3f},\n", nm, threads, (double)threads * iters * 16 / cyc);
     }
   }
   // ---- warp intrinsics
