@@ -11,13 +11,17 @@
 //   PAIRS of same-channel neighbours: key = (bin(a) << LOGB) | bin(b) into a
 //   lane-private table tab[c][key][lane] (bank == lane: conflict-free for any
 //   content) with one red.shared.add per pair, i.e. 0.5 shared atomics per
-//   byte. K0 measured 14.5 conflict-free lane-atomics/clk/SM on B200, so a
-//   per-byte scheme caps at ~62% of the HBM copy peak; pairs lift the cap
-//   above the HBM read rate. On a frame change the CTA's consumer warps
+//   byte. Pairs halve the atomics and the issue slots per byte against a
+//   single key per byte; measured on B200 (profiles/r01_tune.jsonl) pairs
+//   sustain 6.3-6.4 TB/s vs 5.6-5.8 TB/s for one key per byte at B = 16
+//   (the shared-atomic pipe itself, 31.8 lane-ops/clk/SM by the ILP K0
+//   microbenchmark, is not the bound). On a frame change the CTA's consumer warps
 //   marginalise the table (sum over lanes and the partner bin) into 3*B
 //   counters and merge them with one red.global.add each ("one global merge
 //   per block" per frame segment).
-// K2g hist_single_kernel: any bins in [1,256], one atomic per byte, same ring.
+// K2g MODE 1: any bins in [1,256], one atomic per byte, bin = (v*B)>>8, same ring.
+// K2s MODE 4 (NEXT N4): B = 32..256 power of two, one shifted key per byte
+//   (table | bin << 7 | lane << 2), e.g. 256 bins at 6.86 TB/s on C2.
 // K2f hist_ds_kernel<LOGB>: K1+K2 with the 2x box downsample fused into the
 //   consumer (a thread takes the two vertically adjacent 48-byte units of a
 //   row pair, histograms both and emits 8 output pixels), so each sampled
@@ -28,7 +32,7 @@
 //
 // Why not the north_star's per-warp bins + __match_any_sync aggregation: on
 // this B200 MATCH.ANY issues at 0.035 warp-instr/clk/SM (profiles/
-// r01_k0_micro.json), i.e. ~1.1 bytes/clk/SM if applied per byte, ~5% of the
+// r01_k0_micro_v2.json), i.e. ~1.1 bytes/clk/SM if applied per byte, ~5% of the
 // HBM roofline. DESIGN.md §5 records the deviation and the evidence.
 #include "kernels.h"
 #include "ptx.cuh"
