@@ -47,7 +47,49 @@ def main():
     check(w2, ("hist", "shotdiff"), 5)
     check(w2, ("hist", "downsample"), 64)
     check(w1, ("hist", "shotdiff", "downsample"), 16, host=True)
+    check(w1, ("hist", "shotdiff"), 256)   # NEXT N4 (single shifted key, B = 256)
+    check(w1, ("hist", "shotdiff"), 64)
+    next_rows()
     print("sanitize_run ok")
+
+
+def next_rows():
+    import paper_1805_07339_b200 as scn
+    # N2: stencil before sampling
+    w = Workload("sanN2", 48, 20, 2, 30, ("stride", 4), (), spec_kw={"len_min": 3, "len_max": 7})
+    job = scn_harness.StencilJob(w, -1)
+    out = job.alloc_outputs()
+    job.run(out)
+    torch.cuda.synchronize()
+    ref = oracle.stencil_then_sample(w.spec(), job.part, job.row, -1, w.rows_per_video, 16)
+    assert (out["diff"].cpu().numpy().view(np.uint32)[: job.M] == ref).all()
+    job.close()
+    # N3: adaptive cuts with warmup on a shard
+    w = Workload("sanN3", 64, 36, 2, 40, ("stride", 1), (), spec_kw={"len_min": 5, "len_max": 12})
+    pl = scn_harness.plan(w)
+    M = len(pl[1])
+    meta = scn_harness._build_seq(w)
+    b, e = M // 2 + 3, M
+    wb = scn.scn_seq_warmup_begin(meta, b, 4)
+    scn.scn_seq_destroy(meta)
+    job = scn_harness.DeviceJob(w, wb, e, with_halo=True, plan_=pl)
+    o = job.alloc_outputs(("hist", "shotdiff"), 16)
+    job.run(o, ("hist", "shotdiff"), 16)
+    c = torch.empty(e - b, dtype=torch.uint8, device="cuda")
+    scn.scn_run_adaptive_cuts(job.seq, b, e, 4, o["diff"], 4, 1, 64 * 36 // 8, c)
+    torch.cuda.synchronize()
+    _, D, _ = oracle.run(w.spec(), pl[0], pl[1], pl[2], 0, M, 16)
+    assert (c.cpu().numpy() == oracle.adaptive_cuts(D, pl[2], 4, 4, 1, 64 * 36 // 8)[b:e]).all()
+    job.close()
+    # N1: montage (aligned and unaligned canvases)
+    for ww, cols in ((64, 3), (40, 2)):
+        w = Workload("sanN1", ww, 22, 1, 60, ("stride", 1), (), spec_kw={"len_min": 8, "len_max": 20})
+        pl = scn_harness.plan(w)
+        job = scn_harness.DeviceJob(w, 0, len(pl[1]), with_halo=True, plan_=pl)
+        canvas, pos = scn_harness.shot_montage(job, cols, ww * 22)
+        ref = oracle.montage(w.spec(), pl[0][pos], pl[1][pos], cols)
+        assert (canvas.cpu().numpy() == ref).all()
+        job.close()
 
 
 if __name__ == "__main__":
