@@ -262,14 +262,17 @@ __device__ __forceinline__ uint32_t win4(const uint32_t* w) {
   else return __funnelshift_r(w[I >> 2], w[(I >> 2) + 1], 8 * (I & 3));
 }
 template <int M>
-__device__ __forceinline__ uint32_t ds_sum(const uint32_t* t, const uint32_t* b) {
+__device__ __forceinline__ uint32_t ds_sum(const uint32_t* t, const uint32_t* b) {  // sum + 2, <= 1022
   constexpr int I = 2 * M - (M % 3);
-  return __dp4a(win4<I>(b), 0x01000001u, __dp4a(win4<I>(t), 0x01000001u, 2u)) >> 2;
+  return __dp4a(win4<I>(b), 0x01000001u, __dp4a(win4<I>(t), 0x01000001u, 2u));
 }
+// Packing: two 10-bit sums at 16-bit spacing (one IMAD), >> 2 and mask give two
+// output bytes at bytes 0 and 2; one PRMT interleaves the two halves.
 template <int Q>
 __device__ __forceinline__ uint32_t ds_word4(const uint32_t* t, const uint32_t* b) {
-  return ds_sum<4 * Q>(t, b) | ds_sum<4 * Q + 1>(t, b) << 8 | ds_sum<4 * Q + 2>(t, b) << 16 |
-         ds_sum<4 * Q + 3>(t, b) << 24;
+  const uint32_t t02 = ((ds_sum<4 * Q + 2>(t, b) * 65536u + ds_sum<4 * Q>(t, b)) >> 2) & 0x00FF00FFu;
+  const uint32_t t13 = ((ds_sum<4 * Q + 3>(t, b) * 65536u + ds_sum<4 * Q + 1>(t, b)) >> 2) & 0x00FF00FFu;
+  return __byte_perm(t02, t13, 0x6240);
 }
 __device__ __forceinline__ void ds_unit_dp4a(const uint32_t* t, const uint32_t* b, uint32_t* o) {
   o[0] = ds_word4<0>(t, b); o[1] = ds_word4<1>(t, b); o[2] = ds_word4<2>(t, b);
@@ -417,8 +420,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
                          ? ds_frame_base(p.ds_out, item - p.n_halo, p.height / 2, ow3, pitch, p.ds_cols) +
                                ((int64_t)k * (p.rows_per_tile / 2)) * pitch
                          : nullptr;
-      for (uint32_t u = first; u < npairs; u += kConsThreads) {
-        const uint32_t rp = u / upr, xc = u - rp * upr;
+      // unit pair u -> (row pair rp, column unit xc), advanced incrementally (no per-unit division)
+      const uint32_t dq = (uint32_t)kConsThreads / upr, dr = (uint32_t)kConsThreads - dq * upr;
+      uint32_t rp = first / upr, xc = first - rp * upr;
+      for (uint32_t u = first; u < npairs; u += kConsThreads, rp += dq, xc += dr, (xc >= upr) ? (xc -= upr, ++rp) : 0) {
         const uint32_t a = slot + rp * 2u * rowb + xc * 48u;
         uint32_t wt[12], wb[12], o[6];
         load_unit(a, wt);

@@ -3,12 +3,12 @@ shard (+ the recomputed [-1,0] halo), runs HIST + shot-diff through the 
 ABI, and the result columns are all-gathered (ColumnGather, as in bench.py).
 Rank 0 then recomputes the whole job in one process and compares bit-exactly,
 and checks sampled positions against the oracle. Exit code 0 = pass.
-Usage: torchrun --nproc-per-node G tools/dist_check.py [--backend nccl|gloo] [--config NAME] [--frames N]"""
+Usage: torchrun --nproc-per-node G tests/helpers/dist_check.py [--backend nccl|gloo] [--config NAME] [--frames N]"""
 import argparse
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

@@ -162,3 +162,33 @@ def test_c5_rounds():
         del job, out
     del buf
     _free()
+
+
+def test_max_difference_4k_closed_form():
+    # Q13 bound: D <= 6*W*H fits u32. All-0 then all-255 4K frames: every counter moves,
+    # H = {bin 0: W*H} -> {bin 15: W*H} per channel, so D = 2*W*H*3 exactly (closed form).
+    W, H = 3840, 2160
+    F = W * H * 3
+    buf = torch.empty(2 * F, dtype=torch.uint8, device="cuda")
+    buf[:F].fill_(0)
+    buf[F:].fill_(255)
+    t = scn.scn_table_create(2, W, H, 3, scn.SCN_MEM_DEVICE, buf.data_ptr(), F)
+    s = scn.scn_sample_stride(t, 1)
+    ws = torch.empty(max(scn.scn_seq_device_bytes(s), 16), dtype=torch.uint8, device="cuda")
+    scn.scn_seq_upload(s, ws, ws.numel())
+    hist = torch.empty((2, 3, 16), dtype=torch.int32, device="cuda")
+    diff = torch.empty(2, dtype=torch.int32, device="cuda")
+    scratch = torch.empty(48, dtype=torch.int32, device="cuda")
+    scn.scn_run_hist_shotdiff(s, 0, 2, 16, hist, diff, scratch)
+    torch.cuda.synchronize()
+    h = _u32(hist)
+    assert (h[0, :, 0] == W * H).all() and (h[1, :, 15] == W * H).all() and h.sum() == 6 * W * H
+    assert _u32(diff).tolist() == [0, 6 * W * H]
+    # the shard that starts at position 1 recomputes the halo histogram of position 0
+    scn.scn_run_hist_shotdiff(s, 1, 2, 16, hist, diff, scratch)
+    torch.cuda.synchronize()
+    assert int(_u32(diff)[0]) == 6 * W * H
+    scn.scn_seq_destroy(s)
+    scn.scn_table_destroy(t)
+    del buf
+    _free()

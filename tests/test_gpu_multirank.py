@@ -25,7 +25,7 @@ def _port():
 def test_torchrun_sharded_equals_single(world):
     backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tools", "dist_check.py"),
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "helpers", "dist_check.py"),
            "--backend", backend]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

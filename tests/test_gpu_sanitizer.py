@@ -17,7 +17,7 @@ def test_compute_sanitizer(tool):
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
     cmd = [cs, f"--tool={tool}", "--error-exitcode=9", "--target-processes=all",
-           sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")]
+           sys.executable, os.path.join(ROOT, "tests", "helpers", "sanitize_run.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     tail = (r.stdout + r.stderr)[-4000:]
     assert r.returncode == 0, tail
