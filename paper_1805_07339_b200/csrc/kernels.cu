@@ -8,10 +8,11 @@
 //   copies (cp.async.bulk -> UBLKCP) into a 3-stage shared-memory ring guarded
 //   by full/empty mbarriers. Warps 0-15 consume: each thread takes 48-byte
 //   units (16 pixels, 3 x LDS.128, channel of byte j = j mod 3) and counts
-//   PAIRS of same-channel neighbours: key = (bin(a) << LOGB) | bin(b) into a
-//   lane-private table tab[c][key][lane] (bank == lane: conflict-free for any
-//   content) with one red.shared.add per pair, i.e. 0.5 shared atomics per
-//   byte. Pairs halve the atomics and the issue slots per byte against a
+//   PAIRS of same-channel pixels (p, p+8) — bytes j and j+24, same position in
+//   their words, so one SHF + one LOP3 select makes four keys at once —
+//   key = bin(a) | bin(b) << LOGB into a lane-private table tab[c][key][lane]
+//   (bank == lane: conflict-free for any content) with one red.shared.add per
+//   pair, i.e. 0.5 shared atomics per byte, 91 instructions per 48 bytes. Pairs halve the atomics and the issue slots per byte against a
 //   single key per byte; measured on B200 (profiles/r01_tune.jsonl) pairs
 //   sustain 6.3-6.4 TB/s vs 5.6-5.8 TB/s for one key per byte at B = 16
 //   (the shared-atomic pipe itself, 31.8 lane-ops/clk/SM by the ILP K0
@@ -159,9 +160,50 @@ template <int LOGB, int VAR, int... P>
 __device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
   (pair_unit_step<LOGB, P, VAR>(w, lane4), ...);
 }
+// Word-parallel pairing (default): pixel p pairs with pixel p+8 of the unit, i.e. byte j
+// with byte j+24 — same channel (24 = 0 mod 3) and same position within its word, so
+// one SHF + one LOP3 select builds a word K of four 2*LOGB-bit keys:
+//   K = ((w[k] >> (8-LOGB)) & M1) | ((w[k+6] >> (8-2*LOGB)) & M2)   (M1/M2: per-byte fields)
+// and each key costs one shift + one LOP3 (mask | lane4) to become an address.
+// Which pixels are paired does not matter: the flush adds each key's count to both
+// of its bins (same channel), so the marginals are exact for any same-channel pairing.
+template <int LOGB, int K_, int I>
+__device__ __forceinline__ void wpair_key_step(uint32_t K, uint32_t lane4) {
+  constexpr int J = 4 * K_ + I;  // byte of the first pixel of the pair
+  constexpr int c = J % 3;
+  constexpr int B = 1 << LOGB;
+  constexpr uint32_t kmask = ((1u << (2 * LOGB)) - 1u) << 7;
+  uint32_t x;
+  if constexpr (8 * I >= 7) x = K >> (8 * I - 7);
+  else x = K << (7 - 8 * I);
+  red_shared_add_off<c * B * B * 128>(lop3_and_or<kmask>(x, lane4));
+}
+template <int LOGB, int K_>
+__device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
+  constexpr uint32_t f = (1u << LOGB) - 1u;
+  constexpr uint32_t M1 = f * 0x01010101u, M2 = (f << LOGB) * 0x01010101u;
+  const uint32_t a = w[K_] >> (8 - LOGB);
+  const uint32_t b = (8 - 2 * LOGB) > 0 ? (w[K_ + 6] >> (8 - 2 * LOGB)) : w[K_ + 6];
+  uint32_t Kw;
+  if constexpr (M2 == (~M1)) {
+    // per bit: M1 ? a : b  (LUT for operands (b, a, M1): (0xCC & 0xAA) | (0xF0 & ~0xAA) = 0xD8)
+    asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(Kw) : "r"(b), "r"(a), "n"(M1));
+  } else {
+    Kw = (a & M1) | (b & M2);
+  }
+  wpair_key_step<LOGB, K_, 0>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 1>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 2>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 3>(Kw, lane4);
+}
 template <int LOGB, int VAR = 0>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
-  pair_unit_all<LOGB, VAR & 1>(w, lane4, std::make_integer_sequence<int, 24>{});
+  if constexpr ((VAR & 8) || LOGB == 0) {  // adjacent-pixel pairing (previous default)
+    pair_unit_all<LOGB, VAR & 1>(w, lane4, std::make_integer_sequence<int, 24>{});
+  } else {
+    wpair_word<LOGB, 0>(w, lane4); wpair_word<LOGB, 1>(w, lane4); wpair_word<LOGB, 2>(w, lane4);
+    wpair_word<LOGB, 3>(w, lane4); wpair_word<LOGB, 4>(w, lane4); wpair_word<LOGB, 5>(w, lane4);
+  }
 }
 
 // Single-key lane-private counting for B = 2^LOGB in [32, 256] (NEXT N4): byte J of
@@ -713,6 +755,7 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
         if (g_tune_var == 1) return launch_tma<0, 4, 16, 1>(p, st);
         if (g_tune_var == 2) return launch_tma<0, 4, 16, 2>(p, st);
         if (g_tune_var == 3) return launch_tma<0, 4, 16, 3>(p, st);
+        if (g_tune_var == 8) return launch_tma<0, 4, 16, 8>(p, st);
         return launch_tma<0, 4>(p, st);
     }
   }
