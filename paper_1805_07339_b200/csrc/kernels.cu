@@ -127,13 +127,11 @@ __device__ __forceinline__ uint32_t bin_field(const uint32_t* w) {
 }
 
 // Byte J of the unit shifted so its top LOGB bits (its bin) land at bit DST (unmasked).
-// VAR 1 moves right shifts to the FMA pipe (mul.hi by 2^(32-s)), balancing ALU and FMA.
-template <int J, int DST, int LOGB, int VAR = 0>
+template <int J, int DST, int LOGB>
 __device__ __forceinline__ uint32_t bin_shift(const uint32_t* w) {
   constexpr int src = 8 * (J & 3) + 8 - LOGB;
   const uint32_t x = w[J >> 2];
-  if constexpr (src > DST && VAR == 1) return __umulhi(x, 1u << (32 - (src - DST)));
-  else if constexpr (src >= DST) return x >> (src - DST);
+  if constexpr (src >= DST) return x >> (src - DST);
   else return x << (DST - src);
 }
 // (a & b) | c in one LOP3
@@ -146,19 +144,19 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
 
 // Count the 24 same-channel pixel pairs of one 48-byte unit (16 pixels).
 // lane4 = table base | lane << 2. Pair (2q, 2q+1) of channel c: bytes 6q+c, 6q+3+c.
-template <int LOGB, int P, int VAR = 0>
+template <int LOGB, int P>
 __device__ __forceinline__ void pair_unit_step(const uint32_t* w, uint32_t lane4) {
   constexpr int q = P / 3, c = P % 3;
   constexpr int JA = 6 * q + c, JB = 6 * q + 3 + c;
   constexpr int B = 1 << LOGB;
   // addr = (yA & maskA) | ((yB & maskB) | lane4): two LOP3s (forced; the compiler emits three)
-  const uint32_t lo = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<JB, 7, LOGB, VAR>(w), lane4);
-  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << (7 + LOGB)>(bin_shift<JA, 7 + LOGB, LOGB, VAR>(w), lo);
+  const uint32_t lo = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<JB, 7, LOGB>(w), lane4);
+  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << (7 + LOGB)>(bin_shift<JA, 7 + LOGB, LOGB>(w), lo);
   red_shared_add_off<c * B * B * 128>(addr);
 }
-template <int LOGB, int VAR, int... P>
+template <int LOGB, int... P>
 __device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
-  (pair_unit_step<LOGB, P, VAR>(w, lane4), ...);
+  (pair_unit_step<LOGB, P>(w, lane4), ...);
 }
 // Word-parallel pairing (default): pixel p pairs with pixel p+8 of the unit, i.e. byte j
 // with byte j+24 — same channel (24 = 0 mod 3) and same position within its word, so
@@ -198,8 +196,8 @@ __device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
 }
 template <int LOGB, int VAR = 0>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
-  if constexpr ((VAR & 8) || LOGB == 0) {  // adjacent-pixel pairing (previous default)
-    pair_unit_all<LOGB, VAR & 1>(w, lane4, std::make_integer_sequence<int, 24>{});
+  if constexpr ((VAR & 8) || LOGB == 0) {  // adjacent-pixel pairing (previous default, SCN_HIST_VAR=8)
+    pair_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 24>{});
   } else {
     wpair_word<LOGB, 0>(w, lane4); wpair_word<LOGB, 1>(w, lane4); wpair_word<LOGB, 2>(w, lane4);
     wpair_word<LOGB, 3>(w, lane4); wpair_word<LOGB, 4>(w, lane4); wpair_word<LOGB, 5>(w, lane4);
@@ -489,18 +487,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       rot = (rot + npairs) % kConsThreads;
     } else {
       const uint32_t nunits = len / 48u;
-      uint32_t u0 = first;
-      if constexpr (MODE == 0 && (VAR & 2)) {
-        // two units per iteration: 6 LDS.128 in flight, 48 independent atomics
-        for (; u0 + kConsThreads < nunits; u0 += 2 * kConsThreads) {
-          uint32_t w[12], w2[12];
-          load_unit(slot + u0 * 48u, w);
-          load_unit(slot + (u0 + kConsThreads) * 48u, w2);
-          hist_unit_pair<LOGB, VAR>(w, lane4);
-          hist_unit_pair<LOGB, VAR>(w2, lane4);
-        }
-      }
-      for (uint32_t u = u0; u < nunits; u += kConsThreads) {
+      for (uint32_t u = first; u < nunits; u += kConsThreads) {
         uint32_t w[12];
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == 0) {
@@ -662,11 +649,15 @@ const char* hist_variant_name(int32_t bins) {
 template <int MODE, int LOGB, int NW = kDefaultConsWarps, int VAR = 0>
 static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   auto fn = hist_tma_kernel<MODE, LOGB, NW, VAR>;
-  static int configured = 0;  // per instantiation
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  static unsigned configured = 0;  // per instantiation: bit d = smem opt-in done on device d
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned bit = 1u << (dev & 31);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
     if (e != cudaSuccess) return e;
-    configured = 1;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
   int grid = g_num_sms;
   if (p.total_tiles < grid) grid = (int)p.total_tiles;
@@ -675,9 +666,12 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Tuning knobs (env, read once): SCN_HIST_WARPS in {8,16,24} consumer warps for
-// the B=16 pair kernel, SCN_HIST_TILE tile bytes (multiple of 48). Defaults are
-// the measured best.
+// Tuning knobs (env, read once; defaults are the measured best):
+// SCN_HIST_TILE tile bytes of the B = 16 kernel (multiple of 48), SCN_FUSED_TILE
+// target bytes of the row-pair tiles, SCN_HIST_VAR=8 the previous adjacent-pixel
+// pairing, SCN_HIST_SINGLE=1 one key per byte at B = 16, SCN_DS_VAR=0 the bytewise
+// SWAR downsample, SCN_DS_IMPL=1 the LDG downsample kernel. (Measured and removed:
+// 8/24 consumer warps, right shifts as mul.hi, two units per loop iteration.)
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -685,13 +679,13 @@ static int env_int(const char* name, int dflt) {
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
 static uint32_t g_fused_tile = 0;
-static int g_tune_var = 0;  // SCN_HIST_VAR: 1 = mul.hi shifts, 2 = two units/iteration, 3 = both
+static int g_tune_var = 0;  // SCN_HIST_VAR: 8 = adjacent-pixel pairing
 static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
 static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
-  g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
+  g_tune_warps = kDefaultConsWarps;
   int t = env_int("SCN_HIST_TILE", (int)kTile);
   if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
   g_tune_tile = (uint32_t)t;
@@ -750,11 +744,6 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
           p.table_align = 16u * 128u;
           return launch_tma<4, 4>(p, st);
         }
-        if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
-        if (g_tune_warps == 24) return launch_tma<0, 4, 24>(p, st);
-        if (g_tune_var == 1) return launch_tma<0, 4, 16, 1>(p, st);
-        if (g_tune_var == 2) return launch_tma<0, 4, 16, 2>(p, st);
-        if (g_tune_var == 3) return launch_tma<0, 4, 16, 3>(p, st);
         if (g_tune_var == 8) return launch_tma<0, 4, 16, 8>(p, st);
         return launch_tma<0, 4>(p, st);
     }
