@@ -211,7 +211,14 @@ template <int LOGB, int J>
 __device__ __forceinline__ void single_unit_step(const uint32_t* w, uint32_t lane4) {
   constexpr int c = J % 3;
   constexpr int B = 1 << LOGB;
-  const uint32_t addr = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<J, 7, LOGB>(w), lane4);
+  uint32_t addr;
+  if constexpr (LOGB == 8) {
+    // B = 256: the key is the byte; PRMT zero-extends it (ALU), IMAD scales and adds the
+    // lane offset (FMA pipe): one op on each pipe instead of two ALU ops
+    addr = __byte_perm(w[J >> 2], 0u, 0x4440u + (J & 3)) * 128u + lane4;
+  } else {
+    addr = lop3_and_or<((1u << LOGB) - 1u) << 7>(bin_shift<J, 7, LOGB>(w), lane4);
+  }
   red_shared_add_off<c * B * 128>(addr);
 }
 template <int LOGB, int... J>
