@@ -677,22 +677,24 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
 // SCN_HIST_TILE tile bytes of the B = 16 kernel (multiple of 48), SCN_FUSED_TILE
 // target bytes of the row-pair tiles, SCN_HIST_VAR=8 the previous adjacent-pixel
 // pairing, SCN_HIST_SINGLE=1 one key per byte at B = 16, SCN_DS_VAR=0 the bytewise
-// SWAR downsample, SCN_DS_IMPL=1 the LDG downsample kernel. (Measured and removed:
-// 8/24 consumer warps, right shifts as mul.hi, two units per loop iteration.)
+// SWAR downsample, SCN_DS_IMPL=1 the LDG downsample kernel, SCN_HIST_WARPS (8/12/16)
+// and SCN_FUSED_WARPS (8/12/16) consumer warps. (Measured and removed: 20/24 consumer
+// warps, right shifts as mul.hi, two units per loop iteration.)
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
-static uint32_t g_fused_tile = 0;
+static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per row-pair tile
 static int g_tune_var = 0;  // SCN_HIST_VAR: 8 = adjacent-pixel pairing
 static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
-static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys  // SCN_FUSED_TILE: target bytes per fused (hist+downsample) tile
+static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys
+static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused / ds-only kernels (measured best: 8)
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
-  g_tune_warps = kDefaultConsWarps;
+  g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
   int t = env_int("SCN_HIST_TILE", (int)kTile);
   if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
   g_tune_tile = (uint32_t)t;
@@ -703,6 +705,7 @@ static void read_tuning() {
   g_ds_var = env_int("SCN_DS_VAR", 1);
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
   g_hist_single = env_int("SCN_HIST_SINGLE", 0);
+  g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -752,6 +755,8 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
           return launch_tma<4, 4>(p, st);
         }
         if (g_tune_var == 8) return launch_tma<0, 4, 16, 8>(p, st);
+        if (g_tune_warps == 12) return launch_tma<0, 4, 12>(p, st);
+        if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
         return launch_tma<0, 4>(p, st);
     }
   }
@@ -833,6 +838,8 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     case 2: return launch_tma<2, 2>(p, st);
     case 3: return launch_tma<2, 3>(p, st);
     default:
+      if (g_fused_warps == 8 && g_ds_var == 1) return launch_tma<2, 4, 8, 4>(p, st);
+      if (g_fused_warps == 12 && g_ds_var == 1) return launch_tma<2, 4, 12, 4>(p, st);
       if (g_ds_var == 1) return launch_tma<2, 4, kDefaultConsWarps, 4>(p, st);
       return launch_tma<2, 4>(p, st);
   }
@@ -841,6 +848,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
 // downsample-only TMA ring (MODE 3): same row-pair tiles, no table
 static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
                                  cudaStream_t st, int64_t pitch, int32_t cols) {
+  read_tuning();
   HistJob j{};
   j.ds_pitch = pitch;
   j.ds_cols = cols;
@@ -860,6 +868,7 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   p.total_tiles = n * p.tpf;
   p.table_bytes = 0;
   p.table_align = 128;
+  if (g_ds_var == 1 && g_fused_warps == 8) return launch_tma<3, 4, 8, 4>(p, st);
   if (g_ds_var == 1) return launch_tma<3, 4, kDefaultConsWarps, 4>(p, st);
   return launch_tma<3, 4>(p, st);
 }
