@@ -18,7 +18,10 @@ SYNTH_CUDA := scn_synth/libscn_synth_cuda.so
 ORACLE     := oracle/libscn_oracle.so
 MICRO      := tools/micro/k0
 
-all: $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE)
+DEMO       := examples/scn_demo
+CUDA_HOME  ?= /usr/local/cuda
+
+all: $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(DEMO)
 
 lib: $(LIB)
 oracle: $(ORACLE) $(SYNTH_HOST)
@@ -36,10 +39,15 @@ $(SYNTH_CUDA): scn_synth/synth_cuda.cu scn_synth/synth_host.c scn_synth/scn_synt
 $(ORACLE): oracle/scn_oracle.c scn_synth/synth_host.c scn_synth/scn_synth.h
 	$(CC) $(CFLAGS) oracle/scn_oracle.c scn_synth/synth_host.c -o $@
 
+# a plain C consumer of the ABI (no Python): links libscn.so and the CUDA runtime
+$(DEMO): examples/scn_demo.c include/scn.h $(LIB)
+	$(CC) -O2 -std=c11 -Wall -Iinclude -I$(CUDA_HOME)/include $< -o $@ -L$(PKG) -lscn \
+	  -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
+
 $(MICRO): tools/micro/k0.cu
 	$(NVCC) $(ARCH) -O3 -o $@ $<
 
 clean:
-	rm -f $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(MICRO)
+	rm -f $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(MICRO) $(DEMO)
 
 .PHONY: all lib oracle micro clean

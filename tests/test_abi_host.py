@@ -274,3 +274,11 @@ def test_n1_select_and_gather_positions_match_oracle():
         scn.scn_seq_destroy(x)
     scn.scn_table_destroy(ta)
     scn.scn_table_destroy(tb)
+
+
+def test_plain_c_demo_builds_and_links():
+    # the ABI is usable from plain C: examples/scn_demo.c compiles against include/scn.h and links libscn.so
+    import subprocess
+    r = subprocess.run(["make", "-C", ROOT, "examples/scn_demo"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(os.path.join(ROOT, "examples", "scn_demo"))

@@ -190,3 +190,13 @@ def test_host_pipeline_matches_device():
         np.testing.assert_array_equal(out["ds"].cpu().numpy()[:n], DS)
         hj.close()
         dj.close()
+
+
+def test_plain_c_demo_runs():
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", root, "examples/scn_demo"], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(root, "examples", "scn_demo")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "scn_demo: ok" in r.stdout
