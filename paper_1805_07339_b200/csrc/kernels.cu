@@ -47,7 +47,8 @@ namespace scn {
 constexpr int kDefaultConsWarps = 16;  // consumer warps per CTA (+1 producer warp)
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
                                    // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
-constexpr uint32_t kFusedTile = 64512;  // target bytes per row-pair tile of the downsample kernels (measured)
+constexpr uint32_t kFusedTile = 64512;  // target bytes per row-pair tile, fused hist+downsample (measured)
+constexpr uint32_t kDsTile = 23040;     // downsample-only kernel: no table, so smaller tiles and a deeper ring win
 constexpr int kMaxStages = 8;
 constexpr uint32_t kCtrlBytes = 1024;
 constexpr uint32_t kBarId = 1;     // named barrier among consumer warps
@@ -686,7 +687,8 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
-static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per row-pair tile
+static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per row-pair tile (fused)
+static uint32_t g_ds_tile = 0;     // SCN_DS_TILE: target bytes per row-pair tile (downsample only)
 static int g_tune_var = 0;  // SCN_HIST_VAR: 8 = adjacent-pixel pairing
 static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
@@ -701,6 +703,9 @@ static void read_tuning() {
   int f = env_int("SCN_FUSED_TILE", (int)kFusedTile);
   if (f < 96 || f > 65536) f = (int)kTile;
   g_fused_tile = (uint32_t)f;
+  int dt = env_int("SCN_DS_TILE", (int)kDsTile);
+  if (dt < 96 || dt > 65536) dt = (int)kDsTile;
+  g_ds_tile = (uint32_t)dt;
   g_tune_var = env_int("SCN_HIST_VAR", 0);
   g_ds_var = env_int("SCN_DS_VAR", 1);
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
@@ -860,7 +865,8 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   j.bins = 16;
   HistParams p = base_params(j);
   const int64_t rowb = (int64_t)width * 3;
-  int rpt = (int)(g_fused_tile / rowb) & ~1;
+  int rpt = (int)(g_ds_tile / rowb) & ~1;
+  if (rpt < 2) rpt = 2;
   if (rpt > height) rpt = height + (height & 1);
   p.rows_per_tile = rpt;
   p.tile = (uint32_t)(rpt * rowb);
