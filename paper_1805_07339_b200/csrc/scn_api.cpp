@@ -202,11 +202,16 @@ scn_status scn_seq_concat(const scn_seq* const* parts, int32_t n, scn_seq** out)
   for (int32_t i = 0; i < n; ++i) {
     const scn_seq* p = parts[i];
     const size_t m = p->addr.size();
+    // an input may itself be a concatenation: keep its inner parts (tables, slices)
+    const int32_t base = (int32_t)s->tables.size();
     s->addr.insert(s->addr.end(), p->addr.begin(), p->addr.end());
     s->row.insert(s->row.end(), p->row.begin(), p->row.end());
-    s->part.insert(s->part.end(), m, i);
-    for (size_t j = 0; j < m; ++j) s->seg.push_back(j == 0 ? 1 : 0);
-    s->tables.push_back(p->tables.empty() ? nullptr : p->tables[0]);
+    for (size_t j = 0; j < m; ++j) {
+      s->part.push_back(base + p->part[j]);
+      s->seg.push_back(j == 0 ? 1 : p->seg[j]);
+    }
+    if (p->tables.empty()) s->tables.push_back(nullptr);
+    else s->tables.insert(s->tables.end(), p->tables.begin(), p->tables.end());
   }
   *out = s;
   return SCN_OK;

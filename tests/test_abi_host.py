@@ -282,3 +282,23 @@ def test_plain_c_demo_builds_and_links():
     r = subprocess.run(["make", "-C", ROOT, "examples/scn_demo"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert os.path.exists(os.path.join(ROOT, "examples", "scn_demo"))
+
+
+def test_nested_concat_keeps_inner_tables():
+    ta, tb, tc = _table(6), _table(5), _table(4)
+    qa, qb, qc = (scn.scn_sample_stride(t, 2) for t in (ta, tb, tc))
+    inner = scn.scn_seq_concat([qa, qb])
+    outer = scn.scn_seq_concat([inner, qc])
+    part, row = scn.scn_seq_rows(outer)
+    assert part.tolist() == [0, 0, 0, 1, 1, 1, 2, 2]
+    assert row.tolist() == [0, 2, 4, 0, 2, 4, 0, 2]
+    assert scn.scn_seq_seg_starts(outer).tolist() == [1, 0, 0, 1, 0, 0, 1, 0]
+    # the stencil closure still resolves rows through each inner table (clamp per table)
+    req, pos, nbr = scn.scn_seq_stencil_required(outer, 1)
+    rp, rr = scn.scn_seq_rows(req)
+    assert rr.tolist() == [0, 1, 2, 3, 4, 5, 0, 1, 2, 3, 4, 0, 1, 2, 3]
+    assert rp.tolist() == [0] * 6 + [1] * 5 + [2] * 4
+    for x in (qa, qb, qc, inner, outer, req):
+        scn.scn_seq_destroy(x)
+    for t in (ta, tb, tc):
+        scn.scn_table_destroy(t)
