@@ -21,6 +21,9 @@
 //   counters and merge them with one red.global.add each ("one global merge
 //   per block" per frame segment).
 // K2g MODE 1: any bins in [1,256], one atomic per byte, bin = (v*B)>>8, same ring.
+// K2a MODE 5: the north_star's design, kept selectable (SCN_HIST_IMPL=match) and
+//   measured: per-warp bins, __match_any_sync peer aggregation, leader atomics,
+//   __reduce_add_sync merge, one global add per key per block.
 // K2s MODE 4 (NEXT N4): B = 32..256 power of two, one shifted key per byte
 //   (table | bin << 7 | lane << 2), e.g. 256 bins at 6.86 TB/s on C2.
 // K2f hist_ds_kernel<LOGB>: K1+K2 with the 2x box downsample fused into the
@@ -40,6 +43,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 namespace scn {
@@ -411,6 +415,19 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     if constexpr (MODE == 3) return;
     named_bar(kBarId, kConsThreads);
     uint32_t* orow = out_row(item);
+    if constexpr (MODE == 5) {
+      // merge the per-warp bins: lane l < NW holds warp l's count of key k; __reduce_add_sync
+      // sums them and lane 0 issues the block's one global add per key
+      uint32_t* wbins = reinterpret_cast<uint32_t*>(smem + (L.table - base));
+      for (int k = warp; k < 3 * BP; k += kConsWarps) {
+        uint32_t v = lane < kConsWarps ? wbins[lane * 3 * BP + k] : 0u;
+        if (lane < kConsWarps) wbins[lane * 3 * BP + k] = 0u;
+        v = __reduce_add_sync(0xFFFFFFFFu, v);
+        if (lane == 0 && v) red_global_add(orow + k, v);
+      }
+      named_bar(kBarId, kConsThreads);
+      return;
+    }
     const int rows = kSingle ? 3 * B : 3 * BP * BP;
     for (int r = ctid; r < rows; r += kConsThreads) {
       const uint32_t ra = L.table + (uint32_t)r * 128u;
@@ -500,6 +517,19 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == 0) {
           hist_unit_pair<LOGB, VAR>(w, lane4);
+        } else if constexpr (MODE == 5) {
+          // north_star K2a: per-warp bins, peers found with __match_any_sync, one leader
+          // atomic of popc(peers) per peer group
+          const uint32_t am = __activemask();
+          const uint32_t lt = (1u << lane) - 1u;
+          uint32_t* wb = reinterpret_cast<uint32_t*>(smem + (L.table - base)) + (uint32_t)warp * 3u * BP;
+#pragma unroll
+          for (int j = 0; j < 48; ++j) {
+            const uint32_t v = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+            const uint32_t key = (uint32_t)(j % 3) * BP + (v >> (8 - LOGB));
+            const uint32_t peers = __match_any_sync(am, key);
+            if ((peers & lt) == 0) atomicAdd(wb + key, (uint32_t)__popc(peers));
+          }
         } else if constexpr (MODE == 4) {
           hist_unit_single<LOGB>(w, lane4);
         } else {
@@ -694,6 +724,7 @@ static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (me
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
 static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys
 static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused / ds-only kernels (measured best: 8)
+static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -711,6 +742,10 @@ static void read_tuning() {
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
   g_hist_single = env_int("SCN_HIST_SINGLE", 0);
   g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
+  {
+    const char* impl = getenv("SCN_HIST_IMPL");
+    g_hist_match = impl && strcmp(impl, "match") == 0;
+  }
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -754,6 +789,11 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       case 2: return launch_tma<0, 2>(p, st);
       case 3: return launch_tma<0, 3>(p, st);
       default:
+        if (g_hist_match) {  // north_star K2a: per-warp bins + __match_any_sync (SCN_HIST_IMPL=match)
+          p.table_bytes = (uint32_t)kDefaultConsWarps * 3u * 16u * 4u;
+          p.table_align = 128u;
+          return launch_tma<5, 4>(p, st);
+        }
         if (g_hist_single) {  // single shifted key per byte, 6 KB table (SCN_HIST_SINGLE=1)
           p.table_bytes = 3u * 16u * 128u;
           p.table_align = 16u * 128u;

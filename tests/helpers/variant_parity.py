@@ -1,0 +1,44 @@
+"""Parity of the CURRENT kernel variant (selected by SCN_* env knobs, read once per
+process) against the oracle on small multi-table workloads. Exit 0 = pass."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import scn_harness  # noqa: E402
+import scn_synth  # noqa: E402
+from scn_synth import Workload  # noqa: E402
+
+
+def main():
+    cases = [scn_synth.WORKLOADS["C1"],
+             Workload("v1", 96, 54, 2, 30, ("stride", 3), (), spec_kw={"len_min": 3, "len_max": 9}),
+             Workload("v2", 67, 41, 2, 20, ("stride", 1), (), spec_kw={"len_min": 3, "len_max": 9}),
+             Workload("v3", 640, 49, 1, 9, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 4})]
+    for wl in cases:
+        for mode in ("shots", "uniform"):
+            spec = wl.spec(mode=mode)
+            pl = scn_harness.plan(wl)
+            M = len(pl[1])
+            H, D, DS = oracle.run(spec, pl[0], pl[1], pl[2], 0, M, wl.bins, want_ds=True)
+            job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, spec=spec, plan_=pl)
+            out = job.alloc_outputs(("hist", "shotdiff", "downsample"), wl.bins)
+            for ops, fused in ((("hist", "shotdiff"), True), (("hist", "downsample"), True), (("downsample",), False)):
+                job.run(out, ops, wl.bins, fused=fused)
+                torch.cuda.synchronize()
+                if "hist" in ops:
+                    assert (out["hist"].cpu().numpy().view(np.uint32)[:M] == H).all(), (wl.name, mode, ops)
+                if "shotdiff" in ops:
+                    assert (out["diff"].cpu().numpy().view(np.uint32)[:M] == D).all(), (wl.name, mode, ops)
+                if "downsample" in ops:
+                    assert (out["ds"].cpu().numpy()[:M] == DS).all(), (wl.name, mode, ops)
+            job.close()
+    print("variant_parity ok", {k: v for k, v in os.environ.items() if k.startswith("SCN_")})
+
+
+if __name__ == "__main__":
+    main()
