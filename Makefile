@@ -3,6 +3,7 @@
 #   make oracle     -> CPU oracle only (gcc)
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
+GIT_SHA   := $(shell git rev-parse --short=12 HEAD 2>/dev/null || echo unknown)
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -shared -cudart static
 CC        ?= gcc
 CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra -shared
@@ -28,7 +29,7 @@ oracle: $(ORACLE) $(SYNTH_HOST)
 micro: $(MICRO)
 
 $(LIB): $(LIB_SRCS) $(LIB_HDRS)
-	$(NVCC) $(NVFLAGS) -Iinclude -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_GIT_SHA=\"$(GIT_SHA)\" -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
 
 $(SYNTH_HOST): scn_synth/synth_host.c scn_synth/scn_synth.h
 	$(CC) $(CFLAGS) $< -o $@

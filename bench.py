@@ -417,7 +417,12 @@ def run_b200(args):
     hist_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
     step_ms = [ev[k][0].elapsed_time(ev[k][2]) for k in range(args.steps)]
     t = torch.tensor([total_ms, float(np.mean(hist_ms))], dtype=torch.float64, device=dev)
+    rank_ms = [total_ms / args.steps]
     if world > 1:
+        allr = torch.zeros(world, dtype=torch.float64, device=dev)
+        allr[rank] = total_ms / args.steps
+        dist.all_reduce(allr)  # per-rank ms/step (each rank fills its own slot)
+        rank_ms = allr.cpu().tolist()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max, hist_ms_max = float(t[0]), float(t[1])
     gpu_launches = launches[0]
@@ -519,6 +524,7 @@ def run_b200(args):
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "step_ms_min": float(min(step_ms)), "step_ms_median": float(statistics.median(step_ms)),
+            "rank_ms_per_step": rank_ms, "library": scn.scn_version(),
         }
         print(json.dumps(line), flush=True)
     job.close()

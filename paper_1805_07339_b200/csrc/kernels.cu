@@ -326,13 +326,36 @@ __device__ __forceinline__ uint32_t ds_word4(const uint32_t* t, const uint32_t* 
   const uint32_t t13 = ((ds_sum<4 * Q + 3>(t, b) * 65536u + ds_sum<4 * Q + 1>(t, b)) >> 2) & 0x00FF00FFu;
   return __byte_perm(t02, t13, 0x6240);
 }
+// Funnel-free variant (SCN_DS_VAR=2): a pair (X_i, X_{i+3}) that straddles words k, k+1
+// is summed by two dp4a on the aligned words with single-byte weights (FMA pipe only).
+template <int M>
+__device__ __forceinline__ uint32_t ds_sum2(const uint32_t* t, const uint32_t* b) {  // sum + 2, <= 1022
+  constexpr int I = 2 * M - (M % 3), K = I >> 2, O = I & 3;
+  if constexpr (O == 0) {
+    return __dp4a(t[K], 0x01000001u, __dp4a(b[K], 0x01000001u, 2u));
+  } else {
+    constexpr uint32_t wa = 1u << (8 * O), wb = 1u << (8 * (O - 1));
+    return __dp4a(t[K], wa, __dp4a(t[K + 1], wb, __dp4a(b[K], wa, __dp4a(b[K + 1], wb, 2u))));
+  }
+}
+template <int Q>
+__device__ __forceinline__ uint32_t ds_word4b(const uint32_t* t, const uint32_t* b) {
+  const uint32_t t02 = ((ds_sum2<4 * Q + 2>(t, b) * 65536u + ds_sum2<4 * Q>(t, b)) >> 2) & 0x00FF00FFu;
+  const uint32_t t13 = ((ds_sum2<4 * Q + 3>(t, b) * 65536u + ds_sum2<4 * Q + 1>(t, b)) >> 2) & 0x00FF00FFu;
+  return __byte_perm(t02, t13, 0x6240);
+}
+__device__ __forceinline__ void ds_unit_dp4a_nofunnel(const uint32_t* t, const uint32_t* b, uint32_t* o) {
+  o[0] = ds_word4b<0>(t, b); o[1] = ds_word4b<1>(t, b); o[2] = ds_word4b<2>(t, b);
+  o[3] = ds_word4b<3>(t, b); o[4] = ds_word4b<4>(t, b); o[5] = ds_word4b<5>(t, b);
+}
 __device__ __forceinline__ void ds_unit_dp4a(const uint32_t* t, const uint32_t* b, uint32_t* o) {
   o[0] = ds_word4<0>(t, b); o[1] = ds_word4<1>(t, b); o[2] = ds_word4<2>(t, b);
   o[3] = ds_word4<3>(t, b); o[4] = ds_word4<4>(t, b); o[5] = ds_word4<5>(t, b);
 }
 template <int DSV>
 __device__ __forceinline__ void ds_unit_v(const uint32_t* t, const uint32_t* b, uint32_t* o) {
-  if constexpr (DSV == 1) ds_unit_dp4a(t, b, o);
+  if constexpr (DSV == 2) ds_unit_dp4a_nofunnel(t, b, o);
+  else if constexpr (DSV == 1) ds_unit_dp4a(t, b, o);
   else ds_unit(t, b, o);
 }
 
@@ -498,7 +521,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           hist_unit_pair<LOGB>(wb, lane4);
         }
         if (dsf) {
-          ds_unit_v<(VAR >> 2) & 1>(wt, wb, o);
+          ds_unit_v<(VAR & 16) ? 2 : ((VAR >> 2) & 1)>(wt, wb, o);
           st_global_24(dsf + (int64_t)rp * pitch + xc * 24, o);
         }
       }
@@ -883,6 +906,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     case 2: return launch_tma<2, 2>(p, st);
     case 3: return launch_tma<2, 3>(p, st);
     default:
+      if (g_fused_warps == 8 && g_ds_var == 2) return launch_tma<2, 4, 8, 16>(p, st);
       if (g_fused_warps == 8 && g_ds_var == 1) return launch_tma<2, 4, 8, 4>(p, st);
       if (g_fused_warps == 12 && g_ds_var == 1) return launch_tma<2, 4, 12, 4>(p, st);
       if (g_ds_var == 1) return launch_tma<2, 4, kDefaultConsWarps, 4>(p, st);
@@ -914,6 +938,7 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   p.total_tiles = n * p.tpf;
   p.table_bytes = 0;
   p.table_align = 128;
+  if (g_ds_var == 2 && g_fused_warps == 8) return launch_tma<3, 4, 8, 16>(p, st);
   if (g_ds_var == 1 && g_fused_warps == 8) return launch_tma<3, 4, 8, 4>(p, st);
   if (g_ds_var == 1) return launch_tma<3, 4, kDefaultConsWarps, 4>(p, st);
   return launch_tma<3, 4>(p, st);

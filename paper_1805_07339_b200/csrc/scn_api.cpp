@@ -65,7 +65,10 @@ struct scn_seq {
 extern "C" {
 
 const char* scn_last_error(void) { return g_err.c_str(); }
-const char* scn_version(void) { return "scn-b200 0.1 (sm_100a)"; }
+#ifndef SCN_GIT_SHA
+#define SCN_GIT_SHA "unknown"
+#endif
+const char* scn_version(void) { return "scn-b200 0.1 (sm_100a, " SCN_GIT_SHA ")"; }
 int32_t scn_last_launch_count(void) { return g_launches; }
 
 // ---------------------------------------------------------------------------

@@ -16,6 +16,8 @@ VARIANTS = [
     {"SCN_HIST_SINGLE": "1"},
     {"SCN_HIST_VAR": "8"},
     {"SCN_DS_VAR": "0"},
+    {"SCN_DS_VAR": "1"},
+    {"SCN_DS_VAR": "2"},
     {"SCN_DS_IMPL": "1"},
     {"SCN_HIST_WARPS": "8", "SCN_FUSED_WARPS": "16"},
     {"SCN_HIST_TILE": "15360", "SCN_FUSED_TILE": "23040", "SCN_DS_TILE": "64512"},
