@@ -28,7 +28,8 @@ lib: $(LIB)
 oracle: $(ORACLE) $(SYNTH_HOST)
 micro: $(MICRO)
 
-$(LIB): $(LIB_SRCS) $(LIB_HDRS)
+# .git/logs/HEAD changes with every commit, so the embedded SHA (scn_version) stays current
+$(LIB): $(LIB_SRCS) $(LIB_HDRS) $(wildcard .git/logs/HEAD)
 	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_GIT_SHA=\"$(GIT_SHA)\" -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
 
 $(SYNTH_HOST): scn_synth/synth_host.c scn_synth/scn_synth.h
