@@ -302,3 +302,41 @@ def test_nested_concat_keeps_inner_tables():
         scn.scn_seq_destroy(x)
     for t in (ta, tb, tc):
         scn.scn_table_destroy(t)
+
+
+def test_pipeline_host_validation_without_gpu():
+    F16 = 96
+    host = np.zeros(10 * F16, dtype=np.uint8)
+    t = scn.scn_table_create(10, 8, 4, 3, scn.SCN_MEM_HOST, host, F16)
+    q = scn.scn_sample_stride(t, 1)
+    big = 1 << 30
+
+    def run(**kw):
+        a = dict(s=q, begin=0, end=10, bins=16, ops=scn.SCN_OP_HIST | scn.SCN_OP_SHOTDIFF, d_hist=big,
+                 d_diff=big, d_out=None, d_scratch=big, d_staging=big, staging_bytes=1 << 20)
+        a.update(kw)
+        with pytest.raises(scn.ScnError) as e:
+            scn.scn_run_pipeline_host(a["s"], a["begin"], a["end"], a["bins"], a["ops"], a["d_hist"], a["d_diff"],
+                                      a["d_out"], a["d_scratch"], a["d_staging"], a["staging_bytes"])
+        return e.value.status
+
+    assert run(ops=8) == scn.SCN_EINVAL                      # unknown op bit
+    assert run(ops=scn.SCN_OP_SHOTDIFF) == scn.SCN_EINVAL    # shot-diff needs HIST
+    assert run(bins=0) == scn.SCN_EUNSUPPORTED
+    assert run(end=11) == scn.SCN_ERANGE
+    assert run(begin=5, end=4) == scn.SCN_EINVAL
+    assert run(d_hist=None) == scn.SCN_EINVAL
+    assert run(staging_bytes=100) == scn.SCN_EINVAL          # < header + 2 frames
+    assert run(d_staging=big + 8) == scn.SCN_EINVAL          # not 16-aligned
+    assert run(begin=3, d_scratch=None) == scn.SCN_EINVAL    # halo needs scratch
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)
+    # a sparse host table with an absent row in the range
+    ptrs = np.array([host.ctypes.data + i * F16 if i != 6 else 0 for i in range(10)], dtype=np.uint64)
+    t = scn.scn_table_create(10, 8, 4, 3, scn.SCN_MEM_HOST, None, 0, ptrs)
+    q = scn.scn_sample_stride(t, 1)
+    with pytest.raises(scn.ScnError) as e:
+        scn.scn_run_pipeline_host(q, 0, 10, 16, scn.SCN_OP_HIST, big, None, None, None, big, 1 << 20)
+    assert e.value.status == scn.SCN_ERANGE
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)

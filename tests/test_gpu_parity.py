@@ -200,3 +200,25 @@ def test_plain_c_demo_runs():
     r = subprocess.run([os.path.join(root, "examples", "scn_demo")], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "scn_demo: ok" in r.stdout
+
+
+@pytest.mark.parametrize("ops", [("hist",), ("downsample",), ("hist", "downsample"), ("hist", "shotdiff")])
+def test_host_pipeline_op_combinations(ops):
+    wl = Workload("e2e2", 64, 36, 1, 30, ("stride", 1), ops, spec_kw={"len_min": 4, "len_max": 9})
+    pl = scn_harness.plan(wl)
+    v, r, s = _oracle_positions(wl)
+    H, D, DS = oracle.run(wl.spec(), v, r, s, 7, 30, 16, want_ds=True)
+    hj = scn_harness.HostJob(wl, 7, 30, with_halo="shotdiff" in ops, plan_=pl, staging_frames=4)
+    dj = scn_harness.DeviceJob(wl, 7, 30, with_halo=False, plan_=pl)
+    out = dj.alloc_outputs(("hist", "shotdiff", "downsample"), 16)
+    hj.run(out, ops, 16, stream=torch.cuda.current_stream(), copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    n = 23
+    if "hist" in ops:
+        np.testing.assert_array_equal(_u32(out["hist"])[:n], H)
+    if "shotdiff" in ops:
+        np.testing.assert_array_equal(_u32(out["diff"])[:n], D)
+    if "downsample" in ops:
+        np.testing.assert_array_equal(out["ds"].cpu().numpy()[:n], DS)
+    hj.close()
+    dj.close()
