@@ -75,6 +75,7 @@ struct HistParams {
   uint32_t smem_bytes;
   uint32_t table_bytes;
   uint32_t table_align;
+  int32_t l2_hint;  // 1: TMA loads carry an L2 evict_first policy (SCN_TMA_HINT)
 };
 
 __device__ __forceinline__ uint64_t frame_addr(const FrameSrc& s, int64_t i) {
@@ -409,13 +410,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       uint32_t ph = 0;
       int64_t item = t0 / p.tpf;
       int32_t k = (int32_t)(t0 - item * p.tpf);
+      const uint64_t policy = l2_policy_evict_first();
       for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
         const uint64_t off = (uint64_t)k * p.tile;
         const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
         const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * s, bytes);
-        tma_load_1d(L.slot(s), reinterpret_cast<const void*>(frame_addr(p.src, item) + off), bytes, full0 + 8 * s);
+        const void* src = reinterpret_cast<const void*>(frame_addr(p.src, item) + off);
+        if (p.l2_hint) tma_load_1d_hint(L.slot(s), src, bytes, full0 + 8 * s, policy);  // frames are read once
+        else tma_load_1d(L.slot(s), src, bytes, full0 + 8 * s);
         if (++s == L.stages) { s = 0; ph ^= 1; }
       }
     }
@@ -747,6 +751,7 @@ static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (me
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
 static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys
 static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused / ds-only kernels (measured best: 8)
+static int g_tma_hint = 0;     // SCN_TMA_HINT=1: L2 evict_first policy on the frame loads
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
@@ -765,6 +770,7 @@ static void read_tuning() {
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
   g_hist_single = env_int("SCN_HIST_SINGLE", 0);
   g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
+  g_tma_hint = env_int("SCN_TMA_HINT", 0);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
@@ -786,6 +792,8 @@ static HistParams base_params(const HistJob& j) {
   p.height = j.height;
   p.bins = j.bins;
   p.smem_bytes = (uint32_t)g_smem_optin;
+  read_tuning();
+  p.l2_hint = g_tma_hint;
   return p;
 }
 
