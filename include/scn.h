@@ -154,6 +154,25 @@ scn_status scn_run_shotdiff(const scn_seq* s, int64_t begin, int64_t end, int32_
 scn_status scn_run_hist_shotdiff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t* d_hist,
                                  uint32_t* d_diff, uint32_t* d_scratch, void* stream);
 
+/* HIST + shot-diff with the result all-gather fused in (north_star: "Only the
+ * final per-frame result columns are gathered"): instead of writing this
+ * rank's rows to a local buffer for a later collective, the histogram flush
+ * and the shot-diff kernel write rows [begin,end) straight into every rank's
+ * full result columns. h_hist_dests[g] / h_diff_dests[g] (g < n_dest <= 16)
+ * are device addresses of rank g's [M][3][bins] u32 and [M] u32 columns —
+ * local memory for g == self, CUDA-IPC-mapped peer memory otherwise (NVLink
+ * loads/stores/atomics on a multi-GPU node). The call zeroes this rank's rows
+ * in every destination, accumulates the histogram with red.global.add, reads
+ * its own rows back from h_hist_dests[self] for the [-1,0] stencil (the halo
+ * is recomputed into d_scratch) and stores D into every destination.
+ * Rows owned by other ranks are never touched, so ranks need no
+ * synchronisation until they read the gathered columns (after a barrier).
+ * EINVAL if n_dest outside [1,16], self outside [0,n_dest), or a NULL /
+ * misaligned destination. */
+scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end, int32_t bins,
+                                    const uint64_t* h_hist_dests, const uint64_t* h_diff_dests, int32_t n_dest,
+                                    int32_t self, uint32_t* d_scratch, void* stream);
+
 /* 2x integer box downsample ("downsamples the resulting frames
  * (Resize)"): d_out[j] (u8, [end-begin][H/2][W/2][3]) with
  * O[y][x][c] = (P(2y,2x)+P(2y,2x+1)+P(2y+1,2x)+P(2y+1,2x+1)+2) >> 2; a

@@ -74,6 +74,7 @@ _sig("scn_run_adaptive_cuts", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _u32, _u
 _sig("scn_select_shot_starts", ctypes.c_int, _vp, _i64, _i64, _vp, _u32, _vp, _i64, ctypes.POINTER(_i64))
 _sig("scn_seq_gather_positions", ctypes.c_int, _vp, _vp, _i64, _pp)
 _sig("scn_run_montage", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _i64, _vp)
+_sig("scn_run_hist_shotdiff_to", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp)
 _sig("scn_run_pipeline_host", ctypes.c_int, _vp, _i64, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp)
 
 
@@ -286,6 +287,15 @@ def scn_seq_gather_positions(s, positions):
 def scn_run_montage(s, begin, end, cols, d_canvas, canvas_pitch, stream=None) -> None:
     _check(_lib.scn_run_montage(s, begin, end, cols, _ptr(d_canvas), canvas_pitch, _stream(stream)),
            "scn_run_montage")
+
+
+def scn_run_hist_shotdiff_to(s, begin, end, bins, hist_dests, diff_dests, self_index, d_scratch=None,
+                             stream=None) -> None:
+    """HIST + shot-diff writing rows [begin,end) straight into every rank's result columns."""
+    h = np.ascontiguousarray(hist_dests, dtype=np.uint64)
+    d = np.ascontiguousarray(diff_dests, dtype=np.uint64)
+    _check(_lib.scn_run_hist_shotdiff_to(s, begin, end, bins, h.ctypes.data, d.ctypes.data, len(h), self_index,
+                                         _ptr(d_scratch), _stream(stream)), "scn_run_hist_shotdiff_to")
 
 
 __all__ = [n for n in dir() if n.startswith(("scn_", "SCN_"))] + ["ScnError", "ScnBlock", "LIB_PATH"]

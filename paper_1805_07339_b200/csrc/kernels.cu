@@ -76,6 +76,8 @@ struct HistParams {
   uint32_t table_bytes;
   uint32_t table_align;
   int32_t l2_hint;  // 1: TMA loads carry an L2 evict_first policy (SCN_TMA_HINT)
+  int32_t n_dest;   // > 0: results go to every dest[g] (fused all-gather over peer memory)
+  uint64_t dest[kMaxDest];
 };
 
 __device__ __forceinline__ uint64_t frame_addr(const FrameSrc& s, int64_t i) {
@@ -437,11 +439,20 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   auto out_row = [&](int64_t item) -> uint32_t* {
     return item < p.n_halo ? p.halo_out + item * 3 * B : p.out + (item - p.n_halo) * 3 * B;
   };
+  // add v to counter idx of item's row: locally, or (fused all-gather) into the same row of
+  // every rank's result column through peer memory (NVLink when the dest is on another GPU)
+  auto emit = [&](int64_t item, int idx, uint32_t v) {
+    if (p.n_dest == 0 || item < p.n_halo) {
+      red_global_add(out_row(item) + idx, v);
+    } else {
+      const int64_t off = (item - p.n_halo) * 3 * B + idx;
+      for (int g = 0; g < p.n_dest; ++g) red_global_add(reinterpret_cast<uint32_t*>(p.dest[g]) + off, v);
+    }
+  };
 
   auto flush = [&](int64_t item) {
     if constexpr (MODE == 3) return;
     named_bar(kBarId, kConsThreads);
-    uint32_t* orow = out_row(item);
     if constexpr (MODE == 5) {
       // merge the per-warp bins: lane l < NW holds warp l's count of key k; __reduce_add_sync
       // sums them and lane 0 issues the block's one global add per key
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         uint32_t v = lane < kConsWarps ? wbins[lane * 3 * BP + k] : 0u;
         if (lane < kConsWarps) wbins[lane * 3 * BP + k] = 0u;
         v = __reduce_add_sync(0xFFFFFFFFu, v);
-        if (lane == 0 && v) red_global_add(orow + k, v);
+        if (lane == 0 && v) emit(item, k, v);
       }
       named_bar(kBarId, kConsThreads);
       return;
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       }
       if (sum) {
         if (kSingle) {
-          red_global_add(orow + r, sum);
+          emit(item, r, sum);
         } else {
           const int c = r / (BP * BP), key = r % (BP * BP);
           atomicAdd(&hsum[c * BP + (key >> LOGB)], sum);
@@ -481,7 +492,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       if (ctid < 3 * BP) {
         const uint32_t v = hsum[ctid];
         hsum[ctid] = 0;
-        if (v) red_global_add(orow + ctid, v);
+        if (v) emit(item, ctid, v);
       }
     }
     named_bar(kBarId, kConsThreads);
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         uint32_t v;
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(slot + j));
         const uint32_t bin = (v * (uint32_t)B) >> 8;
-        red_global_add(out_row(item) + (j % 3) * B + bin, 1u);
+        emit(item, (int)((j % 3) * B + bin), 1u);
       }
       rot = (rot + nunits) % kConsThreads;
     }
@@ -794,6 +805,8 @@ static HistParams base_params(const HistJob& j) {
   p.smem_bytes = (uint32_t)g_smem_optin;
   read_tuning();
   p.l2_hint = g_tma_hint;
+  p.n_dest = j.n_dest;
+  for (int g = 0; g < kMaxDest; ++g) p.dest[g] = j.dest[g];
   return p;
 }
 
@@ -1003,6 +1016,54 @@ cudaError_t launch_adaptive_cuts(const uint32_t* diff, const uint8_t* seg, int64
   *launches += 1;
   adaptive_cuts_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(diff, seg, q0, n, warmup, k_num, k_den, floor_,
                                                                       cut);
+  return cudaGetLastError();
+}
+}  // namespace scn
+
+namespace scn {
+__global__ void __launch_bounds__(256) zero_dests_kernel(DestList d, int64_t words) {
+  const int g = blockIdx.y;
+  uint32_t* q = reinterpret_cast<uint32_t*>(d.p[g]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = 0u;
+}
+
+cudaError_t launch_zero_dests(const DestList& d, int64_t words, cudaStream_t st, int* launches) {
+  if (d.n <= 0 || words <= 0) return cudaSuccess;
+  *launches += 1;
+  int64_t bx = (words + 255) / 256;
+  if (bx > 1024) bx = 1024;
+  zero_dests_kernel<<<dim3((unsigned)bx, (unsigned)d.n), 256, 0, st>>>(d, words);
+  return cudaGetLastError();
+}
+
+// K3 with the fused all-gather: D[p] goes to every destination column
+__global__ void __launch_bounds__(256) shotdiff_dests_kernel(const uint32_t* __restrict__ hist,
+                                                              const uint32_t* __restrict__ halo,
+                                                              const uint8_t* __restrict__ seg, int64_t n,
+                                                              int32_t bins, DestList d) {
+  const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pos >= n) return;
+  const int K = 3 * bins;
+  uint32_t s = 0;
+  if (!seg[pos]) {
+    const uint32_t* cur = hist + pos * K;
+    const uint32_t* prev = pos == 0 ? halo : cur - K;
+    for (int i = lane; i < K; i += 32) {
+      const uint32_t a = cur[i], b = prev[i];
+      s += a > b ? a - b : b - a;
+    }
+  }
+  s = __reduce_add_sync(0xFFFFFFFFu, s);
+  if (lane < d.n) reinterpret_cast<uint32_t*>(d.p[lane])[pos] = s;
+}
+
+cudaError_t launch_shotdiff_dests(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
+                                  int32_t bins, const DestList& d, cudaStream_t st, int* launches) {
+  if (n <= 0) return cudaSuccess;
+  *launches += 1;
+  shotdiff_dests_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(hist, halo_row, seg, n, bins, d);
   return cudaGetLastError();
 }
 }  // namespace scn

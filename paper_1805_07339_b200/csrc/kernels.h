@@ -23,7 +23,19 @@ struct HistJob {
   int32_t width, height, bins;
   int64_t ds_pitch;    // bytes between output rows (0: (W/2)*3, contiguous frames)
   int32_t ds_cols;     // > 0: montage, frame i is tile (i / cols, i % cols) of a canvas (NEXT N1)
+  int32_t n_dest;      // > 0: non-halo rows go to every dest[g] (row 0 = item n_halo) instead of out
+  uint64_t dest[16];   // device addresses, local or CUDA-IPC-mapped peer memory (fused all-gather)
 };
+constexpr int kMaxDest = 16;
+struct DestList {
+  int32_t n;
+  uint64_t p[kMaxDest];
+};
+// zero `words` u32 at each destination (peer stores for mapped peers)
+cudaError_t launch_zero_dests(const DestList& d, int64_t words, cudaStream_t st, int* launches);
+// shot-diff over n positions writing D[p] to every d.p[g] + p (u32)
+cudaError_t launch_shotdiff_dests(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
+                                  int32_t bins, const DestList& d, cudaStream_t st, int* launches);
 
 // Histogram (zeroes nothing: the caller memsets out/halo_out first).
 // Returns the number of kernel launches in *launches.

@@ -538,6 +538,58 @@ scn_status scn_run_hist_shotdiff(const scn_seq* s, int64_t begin, int64_t end, i
   return run_diff(s, begin, end, bins, d_hist, halo ? d_scratch : nullptr, d_diff, st);
 }
 
+scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end, int32_t bins,
+                                    const uint64_t* h_hist_dests, const uint64_t* h_diff_dests, int32_t n_dest,
+                                    int32_t self, uint32_t* d_scratch, void* stream) {
+  scn_status rc = check_run(s, begin, end, bins, true);
+  if (rc) return rc;
+  if (n_dest < 1 || n_dest > scn::kMaxDest) return fail(SCN_EINVAL, "n_dest must be in [1,%d]", scn::kMaxDest);
+  if (self < 0 || self >= n_dest) return fail(SCN_EINVAL, "self must be in [0,n_dest)");
+  if (!h_hist_dests || !h_diff_dests) return fail(SCN_EINVAL, "destination lists are NULL");
+  for (int32_t g = 0; g < n_dest; ++g)
+    if (!h_hist_dests[g] || !h_diff_dests[g] || h_hist_dests[g] % 4 || h_diff_dests[g] % 4)
+      return fail(SCN_EINVAL, "destination %d is NULL or misaligned", g);
+  if (end == begin) return SCN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int32_t halo = scn_seq_needs_halo(s, begin);
+  if (halo && !d_scratch) return fail(SCN_EINVAL, "d_scratch needed for the halo histogram");
+  if ((rc = check_resident(s, begin - halo, end))) return rc;
+  const int64_t n = end - begin, K = 3 * (int64_t)bins;
+  // this rank owns rows [begin,end) of every destination: zero them (peer stores), then
+  // the histogram flush accumulates straight into all of them
+  scn::DestList dh{}, dd{};
+  dh.n = dd.n = n_dest;
+  for (int32_t g = 0; g < n_dest; ++g) {
+    dh.p[g] = h_hist_dests[g] + (uint64_t)(begin * K) * sizeof(uint32_t);
+    dd.p[g] = h_diff_dests[g] + (uint64_t)begin * sizeof(uint32_t);
+  }
+  int nl = 0;
+  cudaError_t e = scn::launch_zero_dests(dh, n * K, st, &nl);
+  if (e == cudaSuccess && halo) e = cudaMemsetAsync(d_scratch, 0, (size_t)K * sizeof(uint32_t), st);
+  if (e != cudaSuccess) {
+    g_launches += nl;
+    return cuda_fail(e, "zero destinations");
+  }
+  scn::HistJob j{};
+  j.src.ptrs = d_addr(s) + begin - halo;
+  j.n_items = n + halo;
+  j.n_halo = halo;
+  j.out = reinterpret_cast<uint32_t*>(dh.p[self]);
+  j.halo_out = d_scratch;
+  j.width = s->width;
+  j.height = s->height;
+  j.bins = bins;
+  j.n_dest = n_dest;
+  for (int32_t g = 0; g < n_dest; ++g) j.dest[g] = dh.p[g];
+  e = scn::launch_histogram(j, st, &nl);
+  if (e == cudaSuccess)
+    e = scn::launch_shotdiff_dests(reinterpret_cast<const uint32_t*>(dh.p[self]), halo ? d_scratch : nullptr,
+                                   d_seg(s) + begin, n, bins, dd, st, &nl);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "hist_shotdiff_to launch");
+  return SCN_OK;
+}
+
 scn_status scn_run_downsample(const scn_seq* s, int64_t begin, int64_t end, uint8_t* d_out, void* stream) {
   scn_status rc = check_run(s, begin, end, 0, false);
   if (rc) return rc;

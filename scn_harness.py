@@ -366,3 +366,35 @@ def shot_montage(job: "DeviceJob", cols: int, tau: int, out=None, stream=None):
     finally:
         scn.scn_seq_destroy(kseq)
     return canvas[: (-(-k // cols)) * oh], pos
+
+
+class PeerColumns:
+    """Full result columns (hist [M,3,B], diff [M]) on every rank, with every peer's columns
+    mapped into this process through CUDA IPC (torch.multiprocessing's tensor sharing), so
+    scn_run_hist_shotdiff_to can write each rank's rows into all of them (the fused result
+    all-gather; over NVLink when ranks are on different GPUs)."""
+
+    def __init__(self, M: int, bins: int, dist, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.dist = dist
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.hist = torch.zeros((max(M, 1), 3, bins), dtype=torch.int32, device=device)
+        self.diff = torch.zeros(max(M, 1), dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        objs = [None] * self.world
+        dist.all_gather_object(objs, (reduce_tensor(self.hist), reduce_tensor(self.diff)))
+        self.views = []
+        for g, (h, d) in enumerate(objs):
+            if g == self.rank:
+                self.views.append((self.hist, self.diff))
+            else:
+                self.views.append((h[0](*h[1]), d[0](*d[1])))
+        self.hist_ptrs = [v[0].data_ptr() for v in self.views]
+        self.diff_ptrs = [v[1].data_ptr() for v in self.views]
+
+    def close(self):
+        if self.views is None:
+            return
+        self.views = None
+        torch.cuda.synchronize()
+        self.dist.barrier()  # peers drop their mappings before owners free

@@ -30,3 +30,15 @@ def test_torchrun_sharded_equals_single(world):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "PASS" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torchrun_fused_peer_gather(world):
+    # every rank's own columns hold the whole job after the fused (peer-memory) gather
+    backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "helpers", "p2p_check.py"),
+           "--backend", backend]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("PASS") == world

@@ -222,3 +222,26 @@ def test_host_pipeline_op_combinations(ops):
         np.testing.assert_array_equal(out["ds"].cpu().numpy()[:n], DS)
     hj.close()
     dj.close()
+
+
+def test_fused_gather_local_destinations():
+    # scn_run_hist_shotdiff_to with two local destinations (as ranks' columns): both hold the shard's rows
+    wl = Workload("dst", 96, 54, 3, 40, ("stride", 2), ("hist", "shotdiff"), spec_kw={"len_min": 3, "len_max": 9})
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    H, D, _ = oracle.run(wl.spec(), pl[0], pl[1], pl[2], 0, M, 16)
+    cols = [(torch.full((M, 3, 16), 7, dtype=torch.int32, device="cuda"), torch.full((M,), 7, dtype=torch.int32,
+                                                                                      device="cuda"))
+            for _ in range(2)]
+    scratch = torch.empty(48, dtype=torch.int32, device="cuda")
+    for b, e in ((0, M // 2 + 1), (M // 2 + 1, M)):   # two "ranks" in sequence, each writing its rows everywhere
+        job = scn_harness.DeviceJob(wl, b, e, with_halo=True, plan_=pl)
+        scn.scn_run_hist_shotdiff_to(job.seq, b, e, 16, [c[0].data_ptr() for c in cols],
+                                     [c[1].data_ptr() for c in cols], 0, scratch)
+        torch.cuda.synchronize()
+        job.close()
+    for h, d in cols:
+        np.testing.assert_array_equal(_u32(h), H)
+        np.testing.assert_array_equal(_u32(d), D)
+    with pytest.raises(scn.ScnError):
+        scn.scn_run_hist_shotdiff_to(job.seq, 0, 1, 16, [], [], 0, scratch)
