@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames-per-step", type=int, default=64)
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1 result exchange: NCCL all_gather (default) or fused into the kernels over peer memory")
     ap.add_argument("--cuts", type=int, default=0,
                     help="NEXT N3: add the bounded-state adaptive cut detector with warmup W to the step")
     ap.add_argument("--bins", type=int, default=0, help="override the config's bins per channel (NEXT N4: 256)")
@@ -364,7 +366,11 @@ def run_b200(args):
     do_diff, do_ds = "shotdiff" in wl.ops, "downsample" in wl.ops
     ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
     out = job.alloc_outputs(ops, bins)
-    gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 else None
+    p2p = world > 1 and args.gather == "p2p"
+    if p2p and (do_ds or cut_w or not do_diff):
+        raise SystemExit("--gather p2p covers the hist + shot-diff step only")
+    gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 and not p2p else None
+    peer = scn_harness.PeerColumns(M, bins, dist, dev) if p2p else None
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     launches = [0]
@@ -372,6 +378,14 @@ def run_b200(args):
     def step(k=None):
         if k is not None:
             ev[k][0].record(stream)
+        if peer is not None:  # HIST + shot-diff writing this rank's rows into every rank's columns
+            scn.scn_run_hist_shotdiff_to(job.seq, b, e, bins, peer.hist_ptrs, peer.diff_ptrs, rank, out["scratch"],
+                                         stream)
+            launches[0] += scn.scn_last_launch_count()
+            if k is not None:
+                ev[k][1].record(stream)
+                ev[k][2].record(stream)
+            return
         if do_ds:  # HIST + 2x downsample in one read of each frame (reading Q12)
             scn.scn_run_hist_downsample(job.seq, jb, e, bins, out["hist"], out["ds"], stream)
         else:
@@ -507,7 +521,7 @@ def run_b200(args):
             "config": {"workload": wl.name, "frames": M, "width": wl.width, "height": wl.height, "bins": bins,
                        "sampling": str(wl.sampling[:2] if wl.sampling[0] != "range" else ("range", len(wl.sampling[1]), wl.sampling[2])),
                        "ops": "+".join(ops) + (f"+adaptive_cuts(W={cut_w})" if cut_w else "") +
-                              ("+allgather" if world > 1 else ""),
+                              (("+fused_peer_gather" if p2p else "+nccl_allgather") if world > 1 else ""),
                        "content": args.mode, "parallelism": f"dp{world} contiguous shards + 1-frame halo",
                        "hist_variant": ("tma_pair_lane_private" if bins in (1, 2, 4, 8, 16) else
                                         "tma_single_shift_lane_private" if bins in (32, 64, 128, 256) else
@@ -528,6 +542,8 @@ def run_b200(args):
         }
         print(json.dumps(line), flush=True)
     job.close()
+    if peer is not None:
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
