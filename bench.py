@@ -407,16 +407,15 @@ def run_b200(args):
 
     for _ in range(max(args.warmup, 0)):
         step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
     launches[0] = 0
     props = torch.cuda.get_device_properties(dev)
     gpu_id = f"GPU-{props.uuid}" if getattr(props, "uuid", None) else str(dev_index)
     clocks = ClockSampler(gpu_id)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
     torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()  # timed region bracketed by barrier + synchronize on both sides
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
