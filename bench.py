@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames-per-step", type=int, default=64)
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    ap.add_argument("--round-frames", type=int, default=0,
+                    help="process a rank's shard in rounds of this many positions (input + output > HBM, e.g. C5 "
+                         "at N = 1); generation between rounds is untimed, timed steps are summed over rounds")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1 result exchange: NCCL all_gather (default) or fused into the kernels over peer memory")
     ap.add_argument("--cuts", type=int, default=0,
@@ -321,6 +324,81 @@ def run_montage(args):
     return 0
 
 
+def run_rounds(args):
+    """SURVEY §8(d) residency: a shard larger than HBM is processed in rounds (the paper's I/O
+    packets). Each round materialises its positions (untimed), then W warm-up + K timed
+    steps run over that round; a step of the whole job = the sum of the rounds' step times."""
+    import torch
+
+    import paper_1805_07339_b200 as scn
+    import scn_harness
+    import scn_synth
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = scn_synth.WORKLOADS[args.config]
+    st = torch.cuda.current_stream(dev)
+    pl = scn_harness.plan(wl)
+    M = len(pl[1]) if args.frames <= 0 else min(args.frames, len(pl[1]))
+    pl = tuple(x[:M] for x in pl)
+    K = args.round_frames
+    do_ds, do_diff = "downsample" in wl.ops, "shotdiff" in wl.ops
+    ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
+    round_ms, hist_ms, buf, launches = [], [], None, 0
+    for r0 in range(0, M, K):
+        r1 = min(M, r0 + K)
+        job = scn_harness.DeviceJob(wl, r0, r1, with_halo=True, device=dev, stream=st, plan_=pl, buf=buf,
+                                    spec=wl.spec(mode=args.mode))
+        buf = job.buf
+        out = job.alloc_outputs(ops, wl.bins)
+
+        def step(ev=None):
+            nonlocal launches
+            if ev is not None:
+                ev[0].record(st)
+            if do_ds:
+                scn.scn_run_hist_downsample(job.seq, r0, r1, wl.bins, out["hist"], out["ds"], st)
+            else:
+                scn.scn_run_histogram(job.seq, r0, r1, wl.bins, out["hist"], st)
+            launches += scn.scn_last_launch_count() if ev is not None else 0
+            if ev is not None:
+                ev[1].record(st)
+            if do_diff:
+                scn.scn_run_shotdiff(job.seq, r0, r1, wl.bins, out["hist"], out["diff"], out["scratch"], st)
+                launches += scn.scn_last_launch_count() if ev is not None else 0
+
+        for _ in range(max(args.warmup, 0)):
+            step()
+        torch.cuda.synchronize(dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for k in range(args.steps):
+            step(evs[k])
+        b_.record(st)
+        torch.cuda.synchronize(dev)
+        round_ms.append(a.elapsed_time(b_) / args.steps)
+        hist_ms.append(float(np.mean([x.elapsed_time(y) for x, y in evs])))
+        job.close()
+        del out
+    ms = sum(round_ms)
+    peak, peak_src = load_peaks()
+    F = wl.frame_bytes
+    ds_b = (wl.width // 2) * (wl.height // 2) * 3 if do_ds else 0
+    alg = M * (F + 3 * wl.bins * 4 + ds_b)
+    ach = alg / (sum(hist_ms) / 1e3) / 1e9
+    line = {"metric": METRIC, "value": M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name, "frames": M, "rounds": len(round_ms), "round_frames": K,
+                       "ops": "+".join(ops), "round_ms": round_ms,
+                       "l2": "no flush: inputs per round >> 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_step": alg},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -556,6 +634,8 @@ def main():
         return run_graph_e(args)
     if args.montage > 0:
         return run_montage(args)
+    if args.round_frames > 0 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        return run_rounds(args)
     return run_b200(args)
 
 
