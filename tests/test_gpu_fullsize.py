@@ -192,3 +192,29 @@ def test_max_difference_4k_closed_form():
     scn.scn_table_destroy(t)
     del buf
     _free()
+
+
+@pytest.mark.parametrize("w,h", [(7680, 4320), (12000, 34), (10928, 7)])
+def test_large_frames_all_ops(w, h):
+    # 8K frames (2 rows per fused tile); widths past the row-pair TMA limit (W*6 > 65536) take the
+    # generic downsample path; histogram tiles are byte ranges, so any width works
+    wl = scn_synth.Workload("big", w, h, 1, 3, ("stride", 1), ("hist", "shotdiff", "downsample"),
+                            spec_kw={"len_min": 1, "len_max": 2})
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    H, D, DS = oracle.run(wl.spec(), pl[0], pl[1], pl[2], 0, M, 16, want_ds=True)
+    job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, plan_=pl)
+    out = job.alloc_outputs(("hist", "shotdiff", "downsample"), 16)
+    job.run(out, ("hist", "shotdiff"), 16)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_u32(out["hist"])[:M], H)
+    np.testing.assert_array_equal(_u32(out["diff"])[:M], D)
+    job.run(out, ("hist", "downsample"), 16)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_u32(out["hist"])[:M], H)
+    np.testing.assert_array_equal(out["ds"].cpu().numpy()[:M], DS)
+    job.run(out, ("downsample",), 16, fused=False)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["ds"].cpu().numpy()[:M], DS)
+    job.close()
+    _free()
