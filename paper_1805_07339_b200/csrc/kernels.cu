@@ -498,12 +498,34 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     named_bar(kBarId, kConsThreads);
   };
 
+  // row-pair tiling constants of the downsample modes (unused otherwise)
+  struct {
+    uint32_t rowb, upr, dq, dr, last_rows;
+    float inv_upr;
+    int64_t pitch, ow3, tile_out;
+    uint8_t* ds_frame;
+  } rg{};
+  if constexpr (MODE == 2 || MODE == 3) {
+    rg.rowb = (uint32_t)p.width * 3u;
+    rg.upr = (uint32_t)p.width / 16u;
+    rg.dq = (uint32_t)kConsThreads / rg.upr;
+    rg.dr = (uint32_t)kConsThreads - rg.dq * rg.upr;
+    rg.last_rows = (uint32_t)(p.height - (p.tpf - 1) * p.rows_per_tile);
+    rg.inv_upr = 1.0f / (float)rg.upr;
+    rg.pitch = p.ds_pitch;
+    rg.ow3 = (int64_t)(p.width / 2) * 3;
+    rg.tile_out = (int64_t)(p.rows_per_tile / 2) * rg.pitch;
+  }
   int64_t item = t0 / p.tpf;
   int32_t k = (int32_t)(t0 - item * p.tpf);
   for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
     if (item != cur) {
       if (cur >= 0) flush(cur);
       cur = item;
+      if constexpr (MODE == 2 || MODE == 3) {
+        if (item >= p.n_halo)
+          rg.ds_frame = ds_frame_base(p.ds_out, item - p.n_halo, p.height / 2, rg.ow3, rg.pitch, p.ds_cols);
+      }
     }
     const uint64_t off = (uint64_t)k * p.tile;
     const uint32_t len = (uint32_t)((uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile);
@@ -512,38 +534,37 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
     if constexpr (MODE == 2 || MODE == 3) {
-      // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs
-      const uint32_t rowb = (uint32_t)p.width * 3u;
-      const uint32_t upr = (uint32_t)p.width / 16u;
-      const uint32_t rows = len / rowb;
-      const uint32_t npairs = (rows / 2) * upr;
-      const int64_t ow3 = (int64_t)(p.width / 2) * 3;
-      const int64_t pitch = p.ds_pitch;
-      uint8_t* dsf = (item >= p.n_halo)
-                         ? ds_frame_base(p.ds_out, item - p.n_halo, p.height / 2, ow3, pitch, p.ds_cols) +
-                               ((int64_t)k * (p.rows_per_tile / 2)) * pitch
-                         : nullptr;
-      // unit pair u -> (row pair rp, column unit xc), advanced incrementally (no per-unit division)
-      const uint32_t dq = (uint32_t)kConsThreads / upr, dr = (uint32_t)kConsThreads - dq * upr;
-      uint32_t rp = first / upr, xc = first - rp * upr;
-      for (uint32_t u = first; u < npairs; u += kConsThreads, rp += dq, xc += dr, (xc >= upr) ? (xc -= upr, ++rp) : 0) {
-        const uint32_t a = slot + rp * 2u * rowb + xc * 48u;
+      // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs.
+      // Per-frame constants (rg.*) are hoisted out of the tile loop; rows of the last
+      // tile and the frame's output base are precomputed, so a tile costs no division.
+      const uint32_t rows = (k == p.tpf - 1) ? rg.last_rows : (uint32_t)p.rows_per_tile;
+      const uint32_t npairs = (rows / 2) * rg.upr;
+      uint8_t* dsf = (item >= p.n_halo) ? rg.ds_frame + (int64_t)k * rg.tile_out : nullptr;
+      // unit pair u -> (row pair rp, column unit xc): first / upr by a float reciprocal with an
+      // exact correction, then advanced incrementally (no per-unit division)
+      uint32_t rp = __float2uint_rz(__uint2float_rz(first) * rg.inv_upr);
+      if ((rp + 1) * rg.upr <= first) ++rp;
+      if (rp * rg.upr > first) --rp;
+      uint32_t xc = first - rp * rg.upr;
+      for (uint32_t u = first; u < npairs;
+           u += kConsThreads, rp += rg.dq, xc += rg.dr, (xc >= rg.upr) ? (xc -= rg.upr, ++rp) : 0) {
+        const uint32_t a = slot + rp * 2u * rg.rowb + xc * 48u;
         uint32_t wt[12], wb[12], o[6];
         load_unit(a, wt);
-        load_unit(a + rowb, wb);
+        load_unit(a + rg.rowb, wb);
         if constexpr (MODE == 2) {
           hist_unit_pair<LOGB>(wt, lane4);
           hist_unit_pair<LOGB>(wb, lane4);
         }
         if (dsf) {
           ds_unit_v<(VAR & 16) ? 2 : ((VAR >> 2) & 1)>(wt, wb, o);
-          st_global_24(dsf + (int64_t)rp * pitch + xc * 24, o);
+          st_global_24(dsf + (int64_t)rp * rg.pitch + xc * 24, o);
         }
       }
       if (MODE == 2 && (rows & 1)) {  // odd last row of an odd-height frame: histogram only
-        for (uint32_t u = first; u < upr; u += kConsThreads) {
+        for (uint32_t u = first; u < rg.upr; u += kConsThreads) {
           uint32_t w[12];
-          load_unit(slot + (rows - 1) * rowb + u * 48u, w);
+          load_unit(slot + (rows - 1) * rg.rowb + u * 48u, w);
           hist_unit_pair<LOGB>(w, lane4);
         }
       }
@@ -757,6 +778,7 @@ static int g_tune_warps = -1;
 static uint32_t g_tune_tile = 0;
 static uint32_t g_fused_tile = 0;  // SCN_FUSED_TILE: target bytes per row-pair tile (fused)
 static uint32_t g_ds_tile = 0;     // SCN_DS_TILE: target bytes per row-pair tile (downsample only)
+static uint32_t g_fused_tile_env = 0, g_ds_tile_env = 0;  // explicit overrides (0 = rows_per_tile rule)
 static int g_tune_var = 0;  // SCN_HIST_VAR: 8 = adjacent-pixel pairing
 static int g_ds_var = 1;    // SCN_DS_VAR: 0 = SWAR hi/lo + funnel, 1 = dp4a (measured faster)
 static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kernel
@@ -773,9 +795,11 @@ static void read_tuning() {
   int f = env_int("SCN_FUSED_TILE", (int)kFusedTile);
   if (f < 96 || f > 65536) f = (int)kTile;
   g_fused_tile = (uint32_t)f;
+  g_fused_tile_env = getenv("SCN_FUSED_TILE") ? g_fused_tile : 0;
   int dt = env_int("SCN_DS_TILE", (int)kDsTile);
   if (dt < 96 || dt > 65536) dt = (int)kDsTile;
   g_ds_tile = (uint32_t)dt;
+  g_ds_tile_env = getenv("SCN_DS_TILE") ? g_ds_tile : 0;
   g_tune_var = env_int("SCN_HIST_VAR", 0);
   g_ds_var = env_int("SCN_DS_VAR", 1);
   g_ds_impl = env_int("SCN_DS_IMPL", 0);
@@ -786,6 +810,19 @@ static void read_tuning() {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
   }
+}
+
+// Rows per row-pair tile (measured): the largest even row count whose tiles
+// give `stages` ring stages next to a table of table_bytes, unless that is under 4 rows, in
+// which case the largest even count that still gives 2 stages (1080p fused: 6 rows x 3
+// stages; 4K fused: 4 rows x 2; downsample-only 1080p: 8 rows x 4). An explicit tile size
+// from the environment (env_tile > 0) wins.
+static int rows_per_tile(int64_t rowb, uint32_t table_bytes, int stages, uint32_t env_tile) {
+  if (env_tile) return (int)((int64_t)env_tile / rowb) & ~1;
+  const int64_t ring = (int64_t)g_smem_optin - (int64_t)kCtrlBytes - (int64_t)table_bytes - 2048;
+  int r = (int)(ring / stages / rowb) & ~1;
+  if (r < 4) r = (int)(ring / 2 / rowb) & ~1;
+  return r;
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -901,7 +938,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   const int lb = log2_exact(j.bins);
   const int64_t rowb = (int64_t)j.width * 3;
   read_tuning();
-  int rpt = (int)(g_fused_tile / rowb) & ~1;
+  int rpt = rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env);
   if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
   const bool fused = lb >= 0 && j.width % 16 == 0 && rpt >= 2 && j.n_halo == 0;
   if (!fused) {
@@ -950,7 +987,7 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   j.bins = 16;
   HistParams p = base_params(j);
   const int64_t rowb = (int64_t)width * 3;
-  int rpt = (int)(g_ds_tile / rowb) & ~1;
+  int rpt = rows_per_tile(rowb, 0u, 4, g_ds_tile_env);
   if (rpt < 2) rpt = 2;
   if (rpt > height) rpt = height + (height & 1);
   p.rows_per_tile = rpt;
