@@ -21,6 +21,14 @@
  *   - Determinism: every output is an exact integer function of the input;
  *     it does not depend on the shard boundaries, the launch configuration or
  *     the number of GPUs.
+ *   - Devices: kernels launch on the calling thread's current CUDA device; the
+ *     stream and every device buffer passed to a call must belong to it (peer
+ *     destinations of scn_run_hist_shotdiff_to excepted: those are mapped peer
+ *     addresses). One process per GPU is the intended layout.
+ *   - Threads: a table or sequence may be used by several threads at once for
+ *     runs (runs only read it); creating, uploading or destroying it must not
+ *     race with other use. scn_last_error / scn_last_launch_count are per
+ *     thread.
  */
 #ifndef SCN_H
 #define SCN_H
