@@ -560,6 +560,8 @@ def run_b200(args):
                "h2d_bytes_per_step": int((ee - eb) * wl.frame_bytes),
                "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in h_out.values())),
                "positions_per_step": ne, "ms_per_step": e2e_ms,
+               "h2d_GBps": (ee - eb) * wl.frame_bytes / (e2e_ms / 1e3) / 1e9,
+               "h2d_ceiling_note": "raw pinned H2D on the GPU box measured 55.4-55.6 GB/s (profiles/r01_h2d_ceiling.json)",
                "path": "scn_run_pipeline_host: pinned host frames -> double-buffered H2D (copy stream) -> "
                        "hist+shotdiff kernels -> D2H of hist+diff"}
         hj.close()
