@@ -105,3 +105,19 @@ def test_n1_montage_c2_prefix():
     ref = oracle.montage(wl.spec(), part[pos], row[pos], 4)
     np.testing.assert_array_equal(canvas.cpu().numpy(), ref)
     job.close()
+
+
+def test_shot_montage_example_runs(tmp_path):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "m.ppm"
+    r = subprocess.run([sys.executable, os.path.join(root, "examples", "shot_montage.py"), "--frames", "600",
+                        "--out", str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    data = out.read_bytes()
+    assert data.startswith(b"P6 ")
+    wl = scn_synth.WORKLOADS["C2"]
+    n_shots = 1 + len(wl.spec().cut_rows(0, 600))
+    assert f"{n_shots} shots" in r.stdout
