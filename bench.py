@@ -466,14 +466,18 @@ def run_b200(args):
             return
         if do_ds:  # HIST + 2x downsample in one read of each frame (reading Q12)
             scn.scn_run_hist_downsample(job.seq, jb, e, bins, out["hist"], out["ds"], stream)
+            launches[0] += scn.scn_last_launch_count()
+            if do_diff:
+                scn.scn_run_shotdiff(job.seq, jb, e, bins, out["hist"], out["diff"], out["scratch"], stream)
+                launches[0] += scn.scn_last_launch_count()
+        elif do_diff:  # the shard's halo frame rides in the same histogram launch
+            scn.scn_run_hist_shotdiff(job.seq, jb, e, bins, out["hist"], out["diff"], out["scratch"], stream)
+            launches[0] += scn.scn_last_launch_count()
         else:
             scn.scn_run_histogram(job.seq, jb, e, bins, out["hist"], stream)
-        launches[0] += scn.scn_last_launch_count()
+            launches[0] += scn.scn_last_launch_count()
         if k is not None:
             ev[k][1].record(stream)
-        if do_diff:
-            scn.scn_run_shotdiff(job.seq, jb, e, bins, out["hist"], out["diff"], out["scratch"], stream)
-            launches[0] += scn.scn_last_launch_count()
         if cut_w > 0:
             scn.scn_run_adaptive_cuts(job.seq, b, e, cut_w, out["diff"], 4, 1, wl.width * wl.height // 8, d_cut,
                                       stream)
@@ -589,7 +593,11 @@ def run_b200(args):
         peak, peak_src = load_peaks()
         F = wl.frame_bytes
         ds_b = (wl.width // 2) * (wl.height // 2) * 3 if do_ds else 0
-        alg_bytes = (e - jb) * (F + 3 * bins * 4 + ds_b)  # read each frame once, write counts (+ ds)
+        halo = job.p0 - job.lo  # the recomputed [-1,0] halo frame of this shard (0 or 1)
+        # read each frame once (+ the halo), write counts (+ ds); the timed call also
+        # runs the shot-diff (reads 2 rows, writes 4 B per position) when it is fused in
+        diff_b = (e - jb) * (2 * 3 * bins * 4 + 4) if (do_diff and not do_ds) else 0
+        alg_bytes = (e - jb + halo) * F + (e - jb) * (3 * bins * 4 + ds_b) + diff_b
         achieved = alg_bytes / (hist_ms_max / 1e3) / 1e9
         traffic, tsrc = traffic_from_profile(n, F, "histds" if do_ds else "hist")
         ms_per_step = total_ms_max / args.steps
@@ -608,8 +616,9 @@ def run_b200(args):
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("hist_tma_kernel<2,4,16,4> (scn_run_hist_downsample incl. memset)" if do_ds else
-                                    "hist_tma_kernel<0,4,16,0> (scn_run_histogram incl. its memset)"),
+                         "kernel": ("hist_tma_kernel<2,4,8,4> (scn_run_hist_downsample incl. memset)" if do_ds else
+                                    "hist_tma_kernel<0,4,16,0> + shotdiff_kernel (scn_run_hist_shotdiff incl. "
+                                    "memset)" if do_diff else "hist_tma_kernel<0,4,16,0> (scn_run_histogram)"),
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": hist_ms_max,
                          "peak_source": peak_src, "traffic_source": tsrc},
             "cpu_baseline": cpu,

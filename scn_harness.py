@@ -232,140 +232,37 @@ class HostJob:
 
 class ColumnGather:
     """Final result exchange for N > 1: each rank's shard rows of
-    H [n,3,B] and D [n] are padded to ceil(M/G) rows and all-gathered (NCCL on the
-    GPU box, gloo in the CPU tests); result() trims the padding back out."""
+    H [n,3,B] and D [n] are packed into one padded [ceil(M/G), 3B+1] int32 block and
+    all-gathered in ONE collective (NCCL on the GPU box, gloo in the CPU tests);
+    result() unpacks and trims the padding."""
 
     def __init__(self, M: int, world: int, bins: int, device, dist):
         self.M, self.world, self.bins, self.dist = M, world, bins, dist
         self.rows_pad = -(-M // world) if world else 0
         self.spans = [scn.scn_shard_range(M, world, r) for r in range(world)]
-        self.hist_pad = torch.zeros((self.rows_pad, 3, bins), dtype=torch.int32, device=device)
-        self.diff_pad = torch.zeros(self.rows_pad, dtype=torch.int32, device=device)
-        self.hist_all = torch.empty((self.rows_pad * world, 3, bins), dtype=torch.int32, device=device)
-        self.diff_all = torch.empty(self.rows_pad * world, dtype=torch.int32, device=device)
+        self.K = 3 * bins + 1
+        self.pad = torch.zeros((self.rows_pad, self.K), dtype=torch.int32, device=device)
+        self.all = torch.empty((self.rows_pad * world, self.K), dtype=torch.int32, device=device)
 
     def gather(self, hist, diff, n: int):
-        self.hist_pad[:n].copy_(hist[:n])
+        self.pad[:n, : 3 * self.bins].copy_(hist[:n].reshape(n, 3 * self.bins))
         if diff is not None:
-            self.diff_pad[:n].copy_(diff[:n])
-        if self.hist_pad.is_cuda and self.dist.get_backend() == "gloo":
+            self.pad[:n, 3 * self.bins].copy_(diff[:n])
+        if self.pad.is_cuda and self.dist.get_backend() == "gloo":
             # test-only path (several ranks sharing one GPU): gloo gathers host copies
-            hp, dp = self.hist_pad.cpu(), self.diff_pad.cpu()
-            ha, da = self.hist_all.cpu(), self.diff_all.cpu()
-            self.dist.all_gather_into_tensor(ha, hp)
-            self.dist.all_gather_into_tensor(da, dp)
-            self.hist_all.copy_(ha)
-            self.diff_all.copy_(da)
+            pa, aa = self.pad.cpu(), self.all.cpu()
+            self.dist.all_gather_into_tensor(aa, pa)
+            self.all.copy_(aa)
             return
-        self.dist.all_gather_into_tensor(self.hist_all, self.hist_pad)
-        self.dist.all_gather_into_tensor(self.diff_all, self.diff_pad)
+        self.dist.all_gather_into_tensor(self.all, self.pad)
 
     def result(self):
         hs, ds = [], []
         for r, (b, e) in enumerate(self.spans):
             o = r * self.rows_pad
-            hs.append(self.hist_all[o:o + e - b])
-            ds.append(self.diff_all[o:o + e - b])
+            hs.append(self.all[o:o + e - b, : 3 * self.bins].reshape(e - b, 3, self.bins))
+            ds.append(self.all[o:o + e - b, 3 * self.bins])
         return torch.cat(hs), torch.cat(ds)
-
-
-
-class StencilJob:
-    """NEXT N2 (fig:sampling-e): table -> HIST -> [offset,0] stencil -> Sample, over positions
-    [p0, p1) of a workload's sampled sequence. Only the exact required set R = S U clamp(S+offset)
-     is materialised; one scn_run_histogram over R and one scn_run_diff_pairs."""
-
-    def __init__(self, wl: scn_synth.Workload, offset: int = -1, device="cuda", stream=None, spec=None):
-        self.wl, self.offset = wl, offset
-        self.device = torch.device(device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        meta = _build_seq(wl)
-        try:
-            req_meta, pos, nbr = scn.scn_seq_stencil_required(meta, offset)
-            rpart, rrow = scn.scn_seq_rows(req_meta)
-            scn.scn_seq_destroy(req_meta)
-            self.part, self.row = scn.scn_seq_rows(meta)
-        finally:
-            scn.scn_seq_destroy(meta)
-        self.M, self.R = len(self.row), len(rrow)
-        self.F16 = ceil16(wl.frame_bytes)
-        self.buf = torch.empty(max(self.R, 1) * self.F16, dtype=torch.uint8, device=self.device)
-        addrs = self.buf.data_ptr() + np.arange(self.R, dtype=np.uint64) * np.uint64(self.F16)
-        self.spec = spec if spec is not None else wl.spec()
-        if self.R:
-            jobs = torch.empty(self.R * scn_synth.job_bytes(), dtype=torch.uint8, device=self.device)
-            self.spec.fill_device(rpart.astype(np.int32), rrow, addrs, jobs.data_ptr(), self.stream.cuda_stream)
-            self.stream.synchronize()
-            del jobs
-        ptrs = {}
-        for j in range(self.R):
-            v = int(rpart[j])
-            if v not in ptrs:
-                ptrs[v] = np.zeros(wl.rows_per_video, dtype=np.uint64)
-            ptrs[v][int(rrow[j])] = addrs[j]
-        zeros = np.zeros(wl.rows_per_video, dtype=np.uint64)
-        self.seq = _build_seq(wl, lambda v: ptrs.get(v, zeros))
-        self.req, pos, nbr = scn.scn_seq_stencil_required(self.seq, offset)
-        self.ws = torch.empty(max(scn.scn_seq_device_bytes(self.req), 16), dtype=torch.uint8, device=self.device)
-        scn.scn_seq_upload(self.req, self.ws, self.ws.numel(), self.stream)
-        self.d_pos = torch.from_numpy(pos).to(self.device)
-        self.d_nbr = torch.from_numpy(nbr).to(self.device)
-        self.stream.synchronize()
-
-    def alloc_outputs(self, bins=None):
-        bins = bins or self.wl.bins
-        return {"hist_req": torch.empty((max(self.R, 1), 3, bins), dtype=torch.int32, device=self.device),
-                "diff": torch.empty(max(self.M, 1), dtype=torch.int32, device=self.device)}
-
-    def run(self, out, bins=None, stream=None):
-        bins = bins or self.wl.bins
-        st = stream if stream is not None else self.stream
-        scn.scn_run_histogram(self.req, 0, self.R, bins, out["hist_req"], st)
-        n = scn.scn_last_launch_count()
-        scn.scn_run_diff_pairs(out["hist_req"], self.d_pos, self.d_nbr, self.M, bins, out["diff"], st)
-        return n + scn.scn_last_launch_count()
-
-    def close(self):
-        for a in ("req", "seq"):
-            if getattr(self, a, None) is not None:
-                scn.scn_seq_destroy(getattr(self, a))
-                setattr(self, a, None)
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
-
-
-def shot_montage(job: "DeviceJob", cols: int, tau: int, out=None, stream=None):
-    """NEXT N1: the two-job film summary over a DeviceJob's positions [p0, p1).
-
-    Job 1: HIST + shot-diff; the D column goes to the host, where the first position of
-    every shot is selected (D > tau or a table start, reading Q5); job 2: Gather those
-    positions and write their 2x downsample as montage tiles. Returns (canvas, positions)."""
-    wl = job.wl
-    st = stream if stream is not None else job.stream
-    if out is None:
-        out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
-    b, e = job.p0, job.p1
-    scn.scn_run_hist_shotdiff(job.seq, b, e, wl.bins, out["hist"], out["diff"], out["scratch"], st)
-    d = torch.empty(max(e - b, 1), dtype=torch.int32, pin_memory=True)
-    d.copy_(out["diff"][: max(e - b, 1)], non_blocking=True)
-    st.synchronize()
-    pos = scn.scn_select_shot_starts(job.seq, b, e, d.numpy().view(np.uint32)[: e - b], tau)
-    kseq = scn.scn_seq_gather_positions(job.seq, pos)
-    try:
-        k = len(pos)
-        ws = torch.empty(max(scn.scn_seq_device_bytes(kseq), 16), dtype=torch.uint8, device=job.device)
-        scn.scn_seq_upload(kseq, ws, ws.numel(), st)
-        oh, ow = wl.height // 2, wl.width // 2
-        canvas = torch.empty((max(-(-k // cols), 1) * oh, cols * ow, 3), dtype=torch.uint8, device=job.device)
-        scn.scn_run_montage(kseq, 0, k, cols, canvas, cols * ow * 3, st)
-        st.synchronize()
-    finally:
-        scn.scn_seq_destroy(kseq)
-    return canvas[: (-(-k // cols)) * oh], pos
 
 
 class PeerColumns:
