@@ -32,7 +32,7 @@ def test_torchrun_sharded_equals_single(world):
     assert "PASS" in r.stdout
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_torchrun_fused_peer_gather(world):
     # every rank's own columns hold the whole job after the fused (peer-memory) gather
     backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
