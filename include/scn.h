@@ -181,6 +181,15 @@ scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end
                                     const uint64_t* h_hist_dests, const uint64_t* h_diff_dests, int32_t n_dest,
                                     int32_t self, uint32_t* d_scratch, void* stream);
 
+/* Peer destinations for scn_run_hist_shotdiff_to: map another process's device
+ * allocation (a 64-byte cudaIpcMemHandle_t exported by its owner, plus the byte
+ * offset of the column inside that allocation) into this process, opened in the
+ * calling thread's CURRENT device context with lazy peer access (NVLink P2P when
+ * the owner is another GPU). *d_base is the mapping to release, *d_ptr = base +
+ * offset. The library allocates nothing: this only maps memory the peer owns. */
+scn_status scn_ipc_import(const void* handle, int64_t offset, uint64_t* d_base, uint64_t* d_ptr);
+scn_status scn_ipc_release(uint64_t d_base);
+
 /* 2x integer box downsample ("downsamples the resulting frames
  * (Resize)"): d_out[j] (u8, [end-begin][H/2][W/2][3]) with
  * O[y][x][c] = (P(2y,2x)+P(2y,2x+1)+P(2y+1,2x)+P(2y+1,2x+1)+2) >> 2; a

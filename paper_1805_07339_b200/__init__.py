@@ -75,6 +75,8 @@ _sig("scn_select_shot_starts", ctypes.c_int, _vp, _i64, _i64, _vp, _u32, _vp, _i
 _sig("scn_seq_gather_positions", ctypes.c_int, _vp, _vp, _i64, _pp)
 _sig("scn_run_montage", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _i64, _vp)
 _sig("scn_run_hist_shotdiff_to", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp)
+_sig("scn_ipc_import", ctypes.c_int, _vp, _i64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64))
+_sig("scn_ipc_release", ctypes.c_int, ctypes.c_uint64)
 _sig("scn_run_pipeline_host", ctypes.c_int, _vp, _i64, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp)
 
 
@@ -296,6 +298,18 @@ def scn_run_hist_shotdiff_to(s, begin, end, bins, hist_dests, diff_dests, self_i
     d = np.ascontiguousarray(diff_dests, dtype=np.uint64)
     _check(_lib.scn_run_hist_shotdiff_to(s, begin, end, bins, h.ctypes.data, d.ctypes.data, len(h), self_index,
                                          _ptr(d_scratch), _stream(stream)), "scn_run_hist_shotdiff_to")
+
+
+def scn_ipc_import(handle: bytes, offset: int):
+    """Map a peer's IPC-exported allocation on the current device -> (base, ptr)."""
+    hb = ctypes.create_string_buffer(bytes(handle), 64)
+    base, ptr = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.scn_ipc_import(hb, offset, ctypes.byref(base), ctypes.byref(ptr)), "scn_ipc_import")
+    return base.value, ptr.value
+
+
+def scn_ipc_release(base: int) -> None:
+    _check(_lib.scn_ipc_release(base), "scn_ipc_release")
 
 
 __all__ = [n for n in dir() if n.startswith(("scn_", "SCN_"))] + ["ScnError", "ScnBlock", "LIB_PATH"]

@@ -590,6 +590,26 @@ scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end
   return SCN_OK;
 }
 
+scn_status scn_ipc_import(const void* handle, int64_t offset, uint64_t* d_base, uint64_t* d_ptr) {
+  if (!handle || !d_base || !d_ptr || offset < 0) return fail(SCN_EINVAL, "NULL argument or negative offset");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  void* base = nullptr;
+  // opened in the CURRENT device's context; peer access to the owner's GPU is enabled lazily
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *d_base = (uint64_t)(uintptr_t)base;
+  *d_ptr = *d_base + (uint64_t)offset;
+  return SCN_OK;
+}
+
+scn_status scn_ipc_release(uint64_t d_base) {
+  if (!d_base) return fail(SCN_EINVAL, "NULL base");
+  cudaError_t e = cudaIpcCloseMemHandle((void*)(uintptr_t)d_base);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return SCN_OK;
+}
+
 scn_status scn_run_downsample(const scn_seq* s, int64_t begin, int64_t end, uint8_t* d_out, void* stream) {
   scn_status rc = check_run(s, begin, end, 0, false);
   if (rc) return rc;

@@ -267,31 +267,59 @@ class ColumnGather:
 
 class PeerColumns:
     """Full result columns (hist [M,3,B], diff [M]) on every rank, with every peer's columns
-    mapped into this process through CUDA IPC (torch.multiprocessing's tensor sharing), so
-    scn_run_hist_shotdiff_to can write each rank's rows into all of them (the fused result
-    all-gather; over NVLink when ranks are on different GPUs)."""
+    mapped into this process, so scn_run_hist_shotdiff_to can write each rank's rows into all
+    of them (the fused result all-gather; NVLink P2P when ranks are on different GPUs).
+    Export: torch's storage sharing gives the allocation's cudaIpcMemHandle and the column's
+    byte offset; import: scn_ipc_import opens it in THIS rank's device context with lazy peer
+    access."""
 
     def __init__(self, M: int, bins: int, dist, device):
-        from torch.multiprocessing.reductions import reduce_tensor
         self.dist = dist
         self.world, self.rank = dist.get_world_size(), dist.get_rank()
         self.hist = torch.zeros((max(M, 1), 3, bins), dtype=torch.int32, device=device)
         self.diff = torch.zeros(max(M, 1), dtype=torch.int32, device=device)
         torch.cuda.synchronize(device)
+
+        def export(t):
+            st = t.untyped_storage()
+            _, handle, _, off = st._share_cuda_()[:4]
+            handle = bytes(handle)
+            # torch prefixes the 64-byte cudaIpcMemHandle_t with [version byte] + a segment-type byte
+            # ('c' = plain cudaMalloc segment; expandable segments use another format)
+            tag_at = len(handle) - 65
+            if tag_at in (0, 1):
+                if handle[tag_at:tag_at + 1] != b"c":
+                    raise RuntimeError(f"PeerColumns needs cudaMalloc segments (handle tag "
+                                       f"{handle[tag_at:tag_at + 1]!r}); unset expandable_segments")
+                handle = handle[tag_at + 1:]
+            if len(handle) != 64:
+                raise RuntimeError(f"unexpected CUDA IPC handle length {len(handle)}")
+            return handle, int(off) + t.storage_offset() * t.element_size()
+
         objs = [None] * self.world
-        dist.all_gather_object(objs, (reduce_tensor(self.hist), reduce_tensor(self.diff)))
-        self.views = []
-        for g, (h, d) in enumerate(objs):
+        dist.all_gather_object(objs, (export(self.hist), export(self.diff)))
+        self.bases = []
+        self.hist_ptrs, self.diff_ptrs = [], []
+        for g, ((hh, ho), (dh, do)) in enumerate(objs):
             if g == self.rank:
-                self.views.append((self.hist, self.diff))
+                self.hist_ptrs.append(self.hist.data_ptr())
+                self.diff_ptrs.append(self.diff.data_ptr())
+                continue
+            bh, ph = scn.scn_ipc_import(hh, ho)
+            self.bases.append(bh)
+            if dh == hh:  # both columns in one caching-allocator block: one mapping serves both
+                pd = bh + do
             else:
-                self.views.append((h[0](*h[1]), d[0](*d[1])))
-        self.hist_ptrs = [v[0].data_ptr() for v in self.views]
-        self.diff_ptrs = [v[1].data_ptr() for v in self.views]
+                bd, pd = scn.scn_ipc_import(dh, do)
+                self.bases.append(bd)
+            self.hist_ptrs.append(ph)
+            self.diff_ptrs.append(pd)
 
     def close(self):
-        if self.views is None:
+        if self.bases is None:
             return
-        self.views = None
         torch.cuda.synchronize()
+        for b in self.bases:
+            scn.scn_ipc_release(b)
+        self.bases = None
         self.dist.barrier()  # peers drop their mappings before owners free
