@@ -265,6 +265,104 @@ class ColumnGather:
         return torch.cat(hs), torch.cat(ds)
 
 
+class StencilJob:
+    """NEXT N2 (fig:sampling-e): table -> HIST -> [offset,0] stencil -> Sample, over positions
+    [p0, p1) of a workload's sampled sequence. Only the exact required set R = S U clamp(S+offset)
+     is materialised; one scn_run_histogram over R and one scn_run_diff_pairs."""
+
+    def __init__(self, wl: scn_synth.Workload, offset: int = -1, device="cuda", stream=None, spec=None):
+        self.wl, self.offset = wl, offset
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        meta = _build_seq(wl)
+        try:
+            req_meta, pos, nbr = scn.scn_seq_stencil_required(meta, offset)
+            rpart, rrow = scn.scn_seq_rows(req_meta)
+            scn.scn_seq_destroy(req_meta)
+            self.part, self.row = scn.scn_seq_rows(meta)
+        finally:
+            scn.scn_seq_destroy(meta)
+        self.M, self.R = len(self.row), len(rrow)
+        self.F16 = ceil16(wl.frame_bytes)
+        self.buf = torch.empty(max(self.R, 1) * self.F16, dtype=torch.uint8, device=self.device)
+        addrs = self.buf.data_ptr() + np.arange(self.R, dtype=np.uint64) * np.uint64(self.F16)
+        self.spec = spec if spec is not None else wl.spec()
+        if self.R:
+            jobs = torch.empty(self.R * scn_synth.job_bytes(), dtype=torch.uint8, device=self.device)
+            self.spec.fill_device(rpart.astype(np.int32), rrow, addrs, jobs.data_ptr(), self.stream.cuda_stream)
+            self.stream.synchronize()
+            del jobs
+        ptrs = {}
+        for j in range(self.R):
+            v = int(rpart[j])
+            if v not in ptrs:
+                ptrs[v] = np.zeros(wl.rows_per_video, dtype=np.uint64)
+            ptrs[v][int(rrow[j])] = addrs[j]
+        zeros = np.zeros(wl.rows_per_video, dtype=np.uint64)
+        self.seq = _build_seq(wl, lambda v: ptrs.get(v, zeros))
+        self.req, pos, nbr = scn.scn_seq_stencil_required(self.seq, offset)
+        self.ws = torch.empty(max(scn.scn_seq_device_bytes(self.req), 16), dtype=torch.uint8, device=self.device)
+        scn.scn_seq_upload(self.req, self.ws, self.ws.numel(), self.stream)
+        self.d_pos = torch.from_numpy(pos).to(self.device)
+        self.d_nbr = torch.from_numpy(nbr).to(self.device)
+        self.stream.synchronize()
+
+    def alloc_outputs(self, bins=None):
+        bins = bins or self.wl.bins
+        return {"hist_req": torch.empty((max(self.R, 1), 3, bins), dtype=torch.int32, device=self.device),
+                "diff": torch.empty(max(self.M, 1), dtype=torch.int32, device=self.device)}
+
+    def run(self, out, bins=None, stream=None):
+        bins = bins or self.wl.bins
+        st = stream if stream is not None else self.stream
+        scn.scn_run_histogram(self.req, 0, self.R, bins, out["hist_req"], st)
+        n = scn.scn_last_launch_count()
+        scn.scn_run_diff_pairs(out["hist_req"], self.d_pos, self.d_nbr, self.M, bins, out["diff"], st)
+        return n + scn.scn_last_launch_count()
+
+    def close(self):
+        for a in ("req", "seq"):
+            if getattr(self, a, None) is not None:
+                scn.scn_seq_destroy(getattr(self, a))
+                setattr(self, a, None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shot_montage(job: "DeviceJob", cols: int, tau: int, out=None, stream=None):
+    """NEXT N1: the two-job film summary over a DeviceJob's positions [p0, p1).
+
+    Job 1: HIST + shot-diff; the D column goes to the host, where the first position of
+    every shot is selected (D > tau or a table start, reading Q5); job 2: Gather those
+    positions and write their 2x downsample as montage tiles. Returns (canvas, positions)."""
+    wl = job.wl
+    st = stream if stream is not None else job.stream
+    if out is None:
+        out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
+    b, e = job.p0, job.p1
+    scn.scn_run_hist_shotdiff(job.seq, b, e, wl.bins, out["hist"], out["diff"], out["scratch"], st)
+    d = torch.empty(max(e - b, 1), dtype=torch.int32, pin_memory=True)
+    d.copy_(out["diff"][: max(e - b, 1)], non_blocking=True)
+    st.synchronize()
+    pos = scn.scn_select_shot_starts(job.seq, b, e, d.numpy().view(np.uint32)[: e - b], tau)
+    kseq = scn.scn_seq_gather_positions(job.seq, pos)
+    try:
+        k = len(pos)
+        ws = torch.empty(max(scn.scn_seq_device_bytes(kseq), 16), dtype=torch.uint8, device=job.device)
+        scn.scn_seq_upload(kseq, ws, ws.numel(), st)
+        oh, ow = wl.height // 2, wl.width // 2
+        canvas = torch.empty((max(-(-k // cols), 1) * oh, cols * ow, 3), dtype=torch.uint8, device=job.device)
+        scn.scn_run_montage(kseq, 0, k, cols, canvas, cols * ow * 3, st)
+        st.synchronize()
+    finally:
+        scn.scn_seq_destroy(kseq)
+    return canvas[: (-(-k // cols)) * oh], pos
+
+
 class PeerColumns:
     """Full result columns (hist [M,3,B], diff [M]) on every rank, with every peer's columns
     mapped into this process, so scn_run_hist_shotdiff_to can write each rank's rows into all
