@@ -75,6 +75,7 @@ struct HistParams {
   uint32_t smem_bytes;
   uint32_t table_bytes;
   uint32_t table_align;
+  uint32_t stage_bytes;  // VAR bit 32: per-slot staging of the tile's downsample output (after its input bytes)
   int32_t l2_hint;  // 1: TMA loads carry an L2 evict_first policy (SCN_TMA_HINT)
   int32_t n_dest;   // > 0: results go to every dest[g] (fused all-gather over peer memory)
   uint64_t dest[kMaxDest];
@@ -100,18 +101,20 @@ struct Layout {
   __device__ __forceinline__ uint32_t slot(int s) const { return ring + (uint32_t)s * stride; }
 };
 
-// Shared-memory layout: 1 KB control block at the bottom, the lane-private table
-// at the highest table_align-aligned address that fits (so bin fields can be
-// OR-ed into its address), and one contiguous ring of tile slots in between.
+// Shared-memory layout: 1 KB control block at the bottom, the lane-private table at
+// the highest table_align-aligned address that fits (so bin fields can be OR-ed into
+// its address), and one contiguous ring of tile slots in between (each slot: the tile's
+// input bytes, then stage_bytes of staged downsample output when the TMA-store path is on).
 __device__ __forceinline__ Layout make_layout(uint32_t base, uint32_t smem_bytes, uint32_t tile, uint32_t tb_bytes,
-                                              uint32_t tb_align) {
+                                              uint32_t tb_align, uint32_t stage_bytes) {
   Layout L;
   L.ctrl = base;
   const uint32_t end = base + smem_bytes;
   L.table = (end - tb_bytes) & ~(tb_align - 1);
   L.ring = (base + kCtrlBytes + 127) & ~127u;
-  L.stride = (tile + 127) & ~127u;
-  L.stages = L.table >= L.ring + tile ? (int)((L.table - L.ring - tile) / L.stride) + 1 : 0;
+  L.stride = ((tile + 127) & ~127u) + ((stage_bytes + 127) & ~127u);
+  const uint32_t need = stage_bytes ? L.stride : tile;  // the last slot's footprint
+  L.stages = L.table >= L.ring + need ? (int)((L.table - L.ring - need) / L.stride) + 1 : 0;
   if (L.stages > kMaxStages) L.stages = kMaxStages;
   if (L.table < base + kCtrlBytes) L.stages = 0;
   return L;
@@ -372,7 +375,8 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) {
 // ---------------------------------------------------------------------------
 // The persistent TMA-ring histogram kernel. MODE 0: pair-key table (B = 2^LOGB
 // <= 16); MODE 1: single-key table, any B (LOGB unused); MODE 2: pair-key +
-// fused downsample; MODE 3: downsample only (no table). VAR bit 2: dp4a downsample.
+// fused downsample; MODE 3: downsample only (no table). VAR bit 2: dp4a downsample;
+// bit 32: downsample output staged in the slot and written by the producer's TMA bulk stores.
 // ---------------------------------------------------------------------------
 template <int MODE, int LOGB, int NW, int VAR = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_constant__ HistParams p) {
@@ -382,18 +386,21 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int BP = 1 << LOGB;
   const uint32_t base = smem_addr(smem);
-  const Layout L = make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align);
+  const Layout L = make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align, p.stage_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   const int B = (MODE == 1) ? p.bins : BP;
   constexpr bool kSingle = (MODE == 1 || MODE == 4);  // one key per byte: flush rows are (c, bin) directly
+  constexpr bool kTmaStore = (MODE == 2 || MODE == 3) && (VAR & 32);  // downsample out via TMA bulk stores
+  const uint32_t sfree0 = L.ctrl + 512;  // kTmaStore: slot's output area read by its bulk store
 
   if (threadIdx.x == 0) {
     if (L.stages < 2) __trap();
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, kConsWarps);
+      if constexpr (kTmaStore) mbar_init(sfree0 + 8 * s, 1);
     }
     fence_mbar_init();
   }
@@ -405,7 +412,66 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   const int64_t t0 = p.total_tiles * blockIdx.x / gridDim.x;
   const int64_t t1 = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
 
-  if (warp == kConsWarps) {
+  if constexpr (kTmaStore) {
+    if (warp == kConsWarps) {
+      // ---- producer with TMA stores: after the consumers release tile q's slot, its staged
+      // downsample output is bulk-stored (one copy per tile, or per output row in a montage),
+      // issued S tiles behind the loads; sfree[s] tells the consumers the copy has read it ----
+      if (lane == 0) {
+        const int S = L.stages;
+        int s = 0;
+        uint32_t ph = 0;
+        int64_t item = t0 / p.tpf;
+        int32_t k = (int32_t)(t0 - item * p.tpf);
+        int64_t sitem = item;  // tile whose output is stored next
+        int32_t sk = k;
+        const uint32_t in_bytes = (p.tile + 127u) & ~127u;
+        const int64_t ow3 = (int64_t)(p.width / 2) * 3;
+        const uint32_t last_rows = (uint32_t)(p.height - (p.tpf - 1) * p.rows_per_tile);
+        const int64_t tile_out = (int64_t)(p.rows_per_tile / 2) * p.ds_pitch;
+        auto store_next = [&](int slot) {
+          if (sitem >= p.n_halo) {
+            const uint32_t orows = ((sk == p.tpf - 1) ? last_rows : (uint32_t)p.rows_per_tile) / 2u;
+            uint8_t* dst = ds_frame_base(p.ds_out, sitem - p.n_halo, p.height / 2, ow3, p.ds_pitch, p.ds_cols) +
+                           (int64_t)sk * tile_out;
+            const uint32_t src = L.slot(slot) + in_bytes;
+            if (p.ds_pitch == ow3) {
+              tma_store_1d(dst, src, orows * (uint32_t)ow3);
+            } else {
+              for (uint32_t r = 0; r < orows; ++r) tma_store_1d(dst + (int64_t)r * p.ds_pitch, src + r * (uint32_t)ow3, (uint32_t)ow3);
+            }
+          }
+          if (++sk == p.tpf) { sk = 0; ++sitem; }
+        };
+        for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
+          const uint64_t off = (uint64_t)k * p.tile;
+          const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
+          const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          const bool wrapped = t - t0 >= S;
+          if (wrapped) store_next(s);  // tile t - S, released just now
+          mbar_arrive_expect_tx(full0 + 8 * s, bytes);
+          tma_load_1d(L.slot(s), reinterpret_cast<const void*>(frame_addr(p.src, item) + off), bytes, full0 + 8 * s);
+          if (wrapped) {
+            bulk_commit();
+            bulk_wait_read<0>();
+            mbar_arrive(sfree0 + 8 * s);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        // drain: the last min(n, S) tiles
+        const int64_t n = t1 - t0;
+        for (int64_t q = t1 - (n < S ? n : S); q < t1; ++q) {
+          const int slot = (int)((q - t0) % S);
+          mbar_wait(empty0 + 8 * slot, (uint32_t)(((q - t0) / S) & 1));
+          store_next(slot);
+        }
+        bulk_commit();
+        bulk_wait_all();
+      }
+      return;
+    }
+  } else if (warp == kConsWarps) {
     // ---------------- producer: one elected lane issues the bulk copies ----------------
     if (lane == 0) {
       int s = 0;
@@ -500,7 +566,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
 
   // row-pair tiling constants of the downsample modes (unused otherwise)
   struct {
-    uint32_t rowb, upr, dq, dr, last_rows;
+    uint32_t rowb, upr, dq, dr, last_rows, in_bytes, ow3s;
     float inv_upr;
     int64_t pitch, ow3, tile_out;
     uint8_t* ds_frame;
@@ -515,6 +581,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     rg.pitch = p.ds_pitch;
     rg.ow3 = (int64_t)(p.width / 2) * 3;
     rg.tile_out = (int64_t)(p.rows_per_tile / 2) * rg.pitch;
+    rg.in_bytes = (p.tile + 127u) & ~127u;
+    rg.ow3s = (uint32_t)rg.ow3;
   }
   int64_t item = t0 / p.tpf;
   int32_t k = (int32_t)(t0 - item * p.tpf);
@@ -530,6 +598,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const uint64_t off = (uint64_t)k * p.tile;
     const uint32_t len = (uint32_t)((uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile);
     mbar_wait(full0 + 8 * s, ph);
+    if constexpr (kTmaStore) {
+      if (t - t0 >= L.stages) mbar_wait(sfree0 + 8 * s, ph ^ 1);  // the slot's previous output is stored
+    }
     const uint32_t slot = L.slot(s);
     const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
@@ -558,7 +629,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
         if (dsf) {
           ds_unit_v<(VAR & 16) ? 2 : ((VAR >> 2) & 1)>(wt, wb, o);
-          st_global_24(dsf + (int64_t)rp * rg.pitch + xc * 24, o);
+          if constexpr (kTmaStore) {  // staged in the slot's output area; the producer bulk-stores the tile
+            const uint32_t d = slot + rg.in_bytes + rp * rg.ow3s + xc * 24u;
+            sts64(d, o[0], o[1]);
+            sts64(d + 8, o[2], o[3]);
+            sts64(d + 16, o[4], o[5]);
+          } else {
+            st_global_24(dsf + (int64_t)rp * rg.pitch + xc * 24, o);
+          }
         }
       }
       if (MODE == 2 && (rows & 1)) {  // odd last row of an odd-height frame: histogram only
@@ -612,6 +690,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       }
       rot = (rot + nunits) % kConsThreads;
     }
+    if constexpr (kTmaStore) fence_proxy_async_smem();  // staged output visible to the bulk store
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
     if (++s == L.stages) { s = 0; ph ^= 1; }
@@ -786,6 +865,7 @@ static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte 
 static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused / ds-only kernels (measured best: 8)
 static int g_tma_hint = 0;     // SCN_TMA_HINT=1: L2 evict_first policy on the frame loads
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
+static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -806,6 +886,7 @@ static void read_tuning() {
   g_hist_single = env_int("SCN_HIST_SINGLE", 0);
   g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
   g_tma_hint = env_int("SCN_TMA_HINT", 0);
+  g_ds_store = env_int("SCN_DS_STORE", 0);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
@@ -817,12 +898,22 @@ static void read_tuning() {
 // which case the largest even count that still gives 2 stages (1080p fused: 6 rows x 3
 // stages; 4K fused: 4 rows x 2; downsample-only 1080p: 8 rows x 4). An explicit tile size
 // from the environment (env_tile > 0) wins.
-static int rows_per_tile(int64_t rowb, uint32_t table_bytes, int stages, uint32_t env_tile) {
+// With the TMA-store path each slot also holds the tile's output (rows/2 rows of 1.5 W
+// bytes), so a row costs rowb + ow3 / 2 bytes of ring.
+static int rows_per_tile(int64_t rowb, uint32_t table_bytes, int stages, uint32_t env_tile, bool staged) {
   if (env_tile) return (int)((int64_t)env_tile / rowb) & ~1;
-  const int64_t ring = (int64_t)g_smem_optin - (int64_t)kCtrlBytes - (int64_t)table_bytes - 2048;
-  int r = (int)(ring / stages / rowb) & ~1;
-  if (r < 4) r = (int)(ring / 2 / rowb) & ~1;
+  const int64_t cost = staged ? rowb + rowb / 4 : rowb;  // one ow3 = rowb / 2 output row per row pair
+  const int64_t ring = (int64_t)g_smem_optin - (int64_t)kCtrlBytes - (int64_t)table_bytes - 2048 - (staged ? 256 * stages : 0);
+  int r = (int)(ring / stages / cost) & ~1;
+  if (r < 4) r = (int)(ring / 2 / cost) & ~1;
   return r;
+}
+
+// TMA bulk stores of the downsample output need every output row segment 16-byte aligned:
+// W % 32 == 0 (rows of 1.5 W bytes, segments of 24-byte units starting at even units),
+// a 16-byte multiple row pitch and a 16-byte aligned output base.
+static bool ds_store_ok(int32_t width, int64_t pitch, const uint8_t* out) {
+  return g_ds_store && width % 32 == 0 && pitch % 16 == 0 && ((uintptr_t)out & 15u) == 0;
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -938,7 +1029,9 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   const int lb = log2_exact(j.bins);
   const int64_t rowb = (int64_t)j.width * 3;
   read_tuning();
-  int rpt = rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env);
+  const int64_t pitch = j.ds_pitch > 0 ? j.ds_pitch : (int64_t)(j.width / 2) * 3;
+  const bool tstore = lb == 4 && g_fused_warps == 8 && g_ds_var == 1 && ds_store_ok(j.width, pitch, j.ds_out);
+  int rpt = rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env, tstore);
   if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
   const bool fused = lb >= 0 && j.width % 16 == 0 && rpt >= 2 && j.n_halo == 0;
   if (!fused) {
@@ -964,6 +1057,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     case 2: return launch_tma<2, 2>(p, st);
     case 3: return launch_tma<2, 3>(p, st);
     default:
+      if (tstore) {
+        p.stage_bytes = (uint32_t)(rpt / 2) * (uint32_t)(j.width / 2) * 3u;
+        return launch_tma<2, 4, 8, 4 | 32>(p, st);
+      }
       if (g_fused_warps == 8 && g_ds_var == 2) return launch_tma<2, 4, 8, 16>(p, st);
       if (g_fused_warps == 8 && g_ds_var == 1) return launch_tma<2, 4, 8, 4>(p, st);
       if (g_fused_warps == 12 && g_ds_var == 1) return launch_tma<2, 4, 12, 4>(p, st);
@@ -987,7 +1084,8 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   j.bins = 16;
   HistParams p = base_params(j);
   const int64_t rowb = (int64_t)width * 3;
-  int rpt = rows_per_tile(rowb, 0u, 4, g_ds_tile_env);
+  const bool tstore = g_fused_warps == 8 && g_ds_var == 1 && ds_store_ok(width, pitch, out);
+  int rpt = rows_per_tile(rowb, 0u, 4, g_ds_tile_env, tstore);
   if (rpt < 2) rpt = 2;
   if (rpt > height) rpt = height + (height & 1);
   p.rows_per_tile = rpt;
@@ -996,6 +1094,10 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   p.total_tiles = n * p.tpf;
   p.table_bytes = 0;
   p.table_align = 128;
+  if (tstore) {
+    p.stage_bytes = (uint32_t)(rpt / 2) * (uint32_t)(width / 2) * 3u;
+    return launch_tma<3, 4, 8, 4 | 32>(p, st);
+  }
   if (g_ds_var == 2 && g_fused_warps == 8) return launch_tma<3, 4, 8, 16>(p, st);
   if (g_ds_var == 1 && g_fused_warps == 8) return launch_tma<3, 4, 8, 4>(p, st);
   if (g_ds_var == 1) return launch_tma<3, 4, kDefaultConsWarps, 4>(p, st);
