@@ -21,8 +21,9 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_torchrun_sharded_equals_single(world):
+    # world 1 runs the packed all-gather through a real NCCL communicator (one rank per GPU)
     backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "helpers", "dist_check.py"),
