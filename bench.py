@@ -620,7 +620,11 @@ def run_b200(args):
                                     "hist_tma_kernel<0,4,16,0> + shotdiff_kernel (scn_run_hist_shotdiff incl. "
                                     "memset)" if do_diff else "hist_tma_kernel<0,4,16,0> (scn_run_histogram)"),
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": hist_ms_max,
-                         "peak_source": peak_src, "traffic_source": tsrc},
+                         "peak_source": peak_src, "traffic_source": tsrc,
+                         # also against the nominal ~8 TB/s, and the second roofline
+                         # (shared-atomic throughput of K2) next to its K0-measured capacity
+                         "peak_nominal": NOMINAL_HBM_GBPS, "frac_nominal": achieved / NOMINAL_HBM_GBPS,
+                         "shared_atomics": atomic_roofline(bins, (e - jb + halo) * F, hist_ms_max, clk)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
@@ -635,6 +639,24 @@ def run_b200(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+NOMINAL_HBM_GBPS = 8000.0  # B200 nominal HBM3e bandwidth (the north_star's "roughly 8 TB/s")
+K0_ATOMS_ILP = 31.8  # conflict-free lane-private red.shared lane-ops / SM-clock (profiles/r01_k0_micro_v2.json)
+
+
+def atomic_roofline(bins, in_bytes, ms, clk):
+    """Shared-atomic side of the histogram: lane-ops per input byte are fixed by the design
+    (0.5 with pair keys at B <= 16, 1 with one key per byte), so the achieved rate per SM-clock
+    follows from the measured time and the median SM clock under load."""
+    per_byte = 0.5 if bins in (1, 2, 4, 8, 16) else 1.0
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz")
+    if not mhz or ms <= 0:
+        return None
+    rate = per_byte * in_bytes / (ms / 1e3) / (148 * mhz * 1e6)
+    return {"lane_ops_per_input_byte": per_byte, "lane_ops_per_sm_clk": rate,
+            "capacity_lane_ops_per_sm_clk": K0_ATOMS_ILP, "frac": rate / K0_ATOMS_ILP,
+            "clock_mhz_used": mhz, "capacity_source": "profiles/r01_k0_micro_v2.json (atoms_ilp_lane_private)"}
 
 
 def main():
