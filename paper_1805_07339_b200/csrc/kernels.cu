@@ -176,18 +176,29 @@ __device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4,
 // and each key costs one shift + one LOP3 (mask | lane4) to become an address.
 // Which pixels are paired does not matter: the flush adds each key's count to both
 // of its bins (same channel), so the marginals are exact for any same-channel pairing.
-template <int LOGB, int K_, int I>
+//
+// B = 16 layout (kPrmtTable): the 256 keys of channels 0 and 1 share 256-byte rows of a
+// 64 KB-aligned block, tab01[key][c][lane], so key byte I of K drops straight into byte 1
+// of the address with ONE PRMT (byte 0 = lane << 2, bytes 2-3 = the block's high bits;
+// c * 128 is the ATOMS immediate); channel 2 keeps 128-byte rows, tab2[key][lane], in the
+// 32 KB after the block (table | key << 7 | lane << 2 + 64 KB: shift + LOP3). 16 of the
+// unit's 24 keys cost one instruction instead of two; the table is still 96 KB.
+template <int LOGB, int K_, int I, bool PRMT>
 __device__ __forceinline__ void wpair_key_step(uint32_t K, uint32_t lane4) {
   constexpr int J = 4 * K_ + I;  // byte of the first pixel of the pair
   constexpr int c = J % 3;
   constexpr int B = 1 << LOGB;
   constexpr uint32_t kmask = ((1u << (2 * LOGB)) - 1u) << 7;
+  if constexpr (PRMT && c < 2) {
+    red_shared_add_off<c * 128>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
+    return;
+  }
   uint32_t x;
   if constexpr (8 * I >= 7) x = K >> (8 * I - 7);
   else x = K << (7 - 8 * I);
-  red_shared_add_off<c * B * B * 128>(lop3_and_or<kmask>(x, lane4));
+  red_shared_add_off<(PRMT ? 65536 : c * B * B * 128)>(lop3_and_or<kmask>(x, lane4));
 }
-template <int LOGB, int K_>
+template <int LOGB, int K_, bool PRMT>
 __device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
   constexpr uint32_t f = (1u << LOGB) - 1u;
   constexpr uint32_t M1 = f * 0x01010101u, M2 = (f << LOGB) * 0x01010101u;
@@ -200,18 +211,19 @@ __device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
   } else {
     Kw = (a & M1) | (b & M2);
   }
-  wpair_key_step<LOGB, K_, 0>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 1>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 2>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 3>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 0, PRMT>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 1, PRMT>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 2, PRMT>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 3, PRMT>(Kw, lane4);
 }
 template <int LOGB, int VAR = 0>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
   if constexpr ((VAR & 8) || LOGB == 0) {  // adjacent-pixel pairing (previous default, SCN_HIST_VAR=8)
     pair_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 24>{});
   } else {
-    wpair_word<LOGB, 0>(w, lane4); wpair_word<LOGB, 1>(w, lane4); wpair_word<LOGB, 2>(w, lane4);
-    wpair_word<LOGB, 3>(w, lane4); wpair_word<LOGB, 4>(w, lane4); wpair_word<LOGB, 5>(w, lane4);
+    constexpr bool P = LOGB == 4 && !(VAR & 64);  // B = 16: PRMT table layout (VAR bit 64: the previous one)
+    wpair_word<LOGB, 0, P>(w, lane4); wpair_word<LOGB, 1, P>(w, lane4); wpair_word<LOGB, 2, P>(w, lane4);
+    wpair_word<LOGB, 3, P>(w, lane4); wpair_word<LOGB, 4, P>(w, lane4); wpair_word<LOGB, 5, P>(w, lane4);
   }
 }
 
@@ -392,6 +404,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   const int B = (MODE == 1) ? p.bins : BP;
   constexpr bool kSingle = (MODE == 1 || MODE == 4);  // one key per byte: flush rows are (c, bin) directly
+  // B = 16 pair keys with word-parallel pairing: the PRMT table layout (see wpair_key_step)
+  constexpr bool kPrmtTable = (MODE == 0 || MODE == 2) && LOGB == 4 && !(VAR & 8) && !(VAR & 64);
   constexpr bool kTmaStore = (MODE == 2 || MODE == 3) && (VAR & 32);  // downsample out via TMA bulk stores
   const uint32_t sfree0 = L.ctrl + 512;  // kTmaStore: slot's output area read by its bulk store
 
@@ -534,7 +548,11 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     }
     const int rows = kSingle ? 3 * B : 3 * BP * BP;
     for (int r = ctid; r < rows; r += kConsThreads) {
-      const uint32_t ra = L.table + (uint32_t)r * 128u;
+      uint32_t ra = L.table + (uint32_t)r * 128u;
+      if constexpr (kPrmtTable) {  // row (c, key): tab01[key][c] for c < 2, tab2[key] after the 64 KB block
+        const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
+        ra = c < 2 ? L.table + key * 256u + c * 128u : L.table + 65536u + key * 128u;
+      }
       uint32_t sum = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -624,8 +642,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         load_unit(a, wt);
         load_unit(a + rg.rowb, wb);
         if constexpr (MODE == 2) {
-          hist_unit_pair<LOGB>(wt, lane4);
-          hist_unit_pair<LOGB>(wb, lane4);
+          hist_unit_pair<LOGB, VAR & 64>(wt, lane4);
+          hist_unit_pair<LOGB, VAR & 64>(wb, lane4);
         }
         if (dsf) {
           ds_unit_v<(VAR & 16) ? 2 : ((VAR >> 2) & 1)>(wt, wb, o);
@@ -643,7 +661,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         for (uint32_t u = first; u < rg.upr; u += kConsThreads) {
           uint32_t w[12];
           load_unit(slot + (rows - 1) * rg.rowb + u * 48u, w);
-          hist_unit_pair<LOGB>(w, lane4);
+          hist_unit_pair<LOGB, VAR & 64>(w, lane4);
         }
       }
       rot = (rot + npairs) % kConsThreads;
@@ -845,7 +863,7 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
 // Tuning knobs (env, read once; defaults are the measured best):
 // SCN_HIST_TILE tile bytes of the B = 16 kernel (multiple of 48), SCN_FUSED_TILE
 // target bytes of the row-pair tiles, SCN_HIST_VAR=8 the previous adjacent-pixel
-// pairing, SCN_HIST_SINGLE=1 one key per byte at B = 16, SCN_DS_VAR=0 the bytewise
+// pairing, SCN_HIST_VAR=64 the pre-PRMT table layout, SCN_HIST_SINGLE=1 one key per byte at B = 16, SCN_DS_VAR=0 the bytewise
 // SWAR downsample, SCN_DS_IMPL=1 the LDG downsample kernel, SCN_HIST_WARPS (8/12/16)
 // and SCN_FUSED_WARPS (8/12/16) consumer warps. (Measured and removed: 20/24 consumer
 // warps, right shifts as mul.hi, two units per loop iteration.)
@@ -954,7 +972,7 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
   if (lb >= 0) {
     const int Bp = 1 << lb;
     p.table_bytes = 3u * Bp * Bp * 128u;
-    p.table_align = (uint32_t)Bp * Bp * 128u;
+    p.table_align = lb == 4 ? 65536u : (uint32_t)Bp * Bp * 128u;  // B = 16: the PRMT layout's 64 KB block
     switch (lb) {
       case 0: return launch_tma<0, 0>(p, st);
       case 1: return launch_tma<0, 1>(p, st);
@@ -972,6 +990,7 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
           return launch_tma<4, 4>(p, st);
         }
         if (g_tune_var == 8) return launch_tma<0, 4, 16, 8>(p, st);
+        if (g_tune_var == 64) return launch_tma<0, 4, 16, 64>(p, st);  // previous table layout (A/B)
         if (g_tune_warps == 12) return launch_tma<0, 4, 12>(p, st);
         if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
         return launch_tma<0, 4>(p, st);
@@ -1049,7 +1068,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   p.total_tiles = p.n_items * p.tpf;
   const int Bp = 1 << lb;
   p.table_bytes = 3u * Bp * Bp * 128u;
-  p.table_align = (uint32_t)Bp * Bp * 128u;
+  p.table_align = lb == 4 ? 65536u : (uint32_t)Bp * Bp * 128u;  // B = 16: the PRMT layout's 64 KB block
   *launches += 1;
   switch (lb) {
     case 0: return launch_tma<2, 0>(p, st);
@@ -1062,6 +1081,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
         return launch_tma<2, 4, 8, 4 | 32>(p, st);
       }
       if (g_fused_warps == 8 && g_ds_var == 2) return launch_tma<2, 4, 8, 16>(p, st);
+      if (g_fused_warps == 8 && g_ds_var == 1 && g_tune_var == 64) return launch_tma<2, 4, 8, 4 | 64>(p, st);
       if (g_fused_warps == 8 && g_ds_var == 1) return launch_tma<2, 4, 8, 4>(p, st);
       if (g_fused_warps == 12 && g_ds_var == 1) return launch_tma<2, 4, 12, 4>(p, st);
       if (g_ds_var == 1) return launch_tma<2, 4, kDefaultConsWarps, 4>(p, st);

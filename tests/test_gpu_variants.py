@@ -1,6 +1,6 @@
 """Every selectable kernel variant (env knobs) stays bit-exact: the
 north_star's per-warp match_any bins (K2a), one key per byte at B = 16, the previous
-adjacent-pixel pairing, the bytewise SWAR downsample, the LDG downsample kernel, the downsample output
+adjacent-pixel pairing, the pre-PRMT table layout, the bytewise SWAR downsample, the LDG downsample kernel, the downsample output
 staged in the ring slot and written by the producer's TMA bulk stores, and
 non-default warp counts / tile sizes."""
 import os
@@ -16,6 +16,7 @@ VARIANTS = [
     {"SCN_HIST_IMPL": "match"},
     {"SCN_HIST_SINGLE": "1"},
     {"SCN_HIST_VAR": "8"},
+    {"SCN_HIST_VAR": "64"},
     {"SCN_DS_VAR": "0"},
     {"SCN_DS_VAR": "1"},
     {"SCN_DS_VAR": "2"},
