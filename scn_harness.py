@@ -133,15 +133,15 @@ class DeviceJob:
         st = stream if stream is not None else self.stream
         s, b, e = self.seq, self.p0, self.p1
         launches = 0
-        if "hist" in ops and "shotdiff" in ops and fused:
-            scn.scn_run_hist_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
-            launches += scn.scn_last_launch_count()
-        elif "hist" in ops and "downsample" in ops and fused:
+        if "hist" in ops and "downsample" in ops and fused:
             scn.scn_run_hist_downsample(s, b, e, bins, out["hist"], out["ds"], st)
             launches += scn.scn_last_launch_count()
             if "shotdiff" in ops:
                 scn.scn_run_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
                 launches += scn.scn_last_launch_count()
+        elif "hist" in ops and "shotdiff" in ops and fused:
+            scn.scn_run_hist_shotdiff(s, b, e, bins, out["hist"], out["diff"], out["scratch"], st)
+            launches += scn.scn_last_launch_count()
         else:
             if "hist" in ops:
                 scn.scn_run_histogram(s, b, e, bins, out["hist"], st)

@@ -88,6 +88,10 @@ def test_small_shapes_all_ops(w, h, bins):
     np.testing.assert_array_equal(got["ds"], DS)
     got = _run(wl, 0, len(r), ("downsample",), bins, fused=False)
     np.testing.assert_array_equal(got["ds"], DS)
+    got = _run(wl, 0, len(r), ("hist", "downsample", "shotdiff"), bins)  # fused hist+ds, then shot-diff
+    np.testing.assert_array_equal(got["hist"], H)
+    np.testing.assert_array_equal(got["diff"], D)
+    np.testing.assert_array_equal(got["ds"], DS)
 
 
 @pytest.mark.parametrize("mode", ["uniform", "constant", "xgrad", "shots"])
