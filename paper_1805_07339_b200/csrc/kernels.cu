@@ -2,7 +2,7 @@
 // hot path (arXiv 1805.07339 P:L331 HIST, P:L455 shot boundaries via
 // histogram differences over a [-1,0] stencil P:L210, P:L183/P:L335 resize).
 //
-// K1+K2 hist_pair_kernel<LOGB>  (bins = 2^LOGB <= 16; the configs' B = 16)
+// K1+K2 hist_tma_kernel<0, LOGB>  (bins = 2^LOGB <= 16; the configs' B = 16)
 //   Persistent, one CTA per SM (227 KB smem). Warp 16 is a TMA producer: one
 //   elected lane streams 43,008-byte tiles of the sampled frames with 1-D bulk
 //   copies (cp.async.bulk -> UBLKCP) into a 3-stage shared-memory ring guarded
@@ -10,9 +10,10 @@
 //   units (16 pixels, 3 x LDS.128, channel of byte j = j mod 3) and counts
 //   PAIRS of same-channel pixels (p, p+8) — bytes j and j+24, same position in
 //   their words, so one SHF + one LOP3 select makes four keys at once —
-//   key = bin(a) | bin(b) << LOGB into a lane-private table tab[c][key][lane]
-//   (bank == lane: conflict-free for any content) with one red.shared.add per
-//   pair, i.e. 0.5 shared atomics per byte, 91 instructions per 48 bytes. Pairs halve the atomics and the issue slots per byte against a
+//   key = bin(a) | bin(b) << LOGB into a lane-private table (bank == lane:
+//   conflict-free for any content; at B = 16 channels 0/1 share 256-byte key rows
+//   so one PRMT turns a key byte into its address) with one red.shared.add per
+//   pair, i.e. 0.5 shared atomics per byte, 75 instructions per 48 bytes. Pairs halve the atomics and the issue slots per byte against a
 //   single key per byte; measured on B200 (profiles/r01_tune.jsonl) pairs
 //   sustain 6.3-6.4 TB/s vs 5.6-5.8 TB/s for one key per byte at B = 16
 //   (the shared-atomic pipe itself, 31.8 lane-ops/clk/SM by the ILP K0
@@ -26,13 +27,14 @@
 //   __reduce_add_sync merge, one global add per key per block.
 // K2s MODE 4 (NEXT N4): B = 32..256 power of two, one shifted key per byte
 //   (table | bin << 7 | lane << 2), e.g. 256 bins at 6.86 TB/s on C2.
-// K2f hist_ds_kernel<LOGB>: K1+K2 with the 2x box downsample fused into the
+// K2f hist_tma_kernel<2, LOGB>: K1+K2 with the 2x box downsample fused into the
 //   consumer (a thread takes the two vertically adjacent 48-byte units of a
 //   row pair, histograms both and emits 8 output pixels), so each sampled
 //   frame is read from HBM once (reading Q12).
 // K3 shotdiff_kernel: one warp per position, L1 over 3*B counters with
 //   __reduce_add_sync.
-// K4 downsample_kernel: LDG.128-vectorised 2x box downsample.
+// K4 hist_tma_kernel<3, 4>: the same ring without the table (downsample only);
+//   downsample_vec_kernel (LDG.128) and downsample_generic_kernel (any W) otherwise.
 //
 // Why not the north_star's per-warp bins + __match_any_sync aggregation: on
 // this B200 MATCH.ANY issues at 0.035 warp-instr/clk/SM (profiles/
