@@ -5,7 +5,9 @@ Contract (driver): `python bench.py --gpus N --steps K --warmup W` (torchrun for
 N > 1) prints ONE JSON line on rank 0. A step is one pass of the whole hot path
 (sample -> per-channel histogram -> [-1,0] shot-diff, + NCCL all-gather of the
 result columns when N > 1) over the BASELINE config C2 (1920x1080 RGB8,
-16,384 frames, Stride 1), frames already resident in HBM. `--impl reference`
+16,384 frames, Stride 1), frames already resident in HBM. Weak scaling by default:
+at N GPUs the film is N x 16,384 frames, split contiguously (each GPU one config's
+worth + its recomputed 1-frame halo); `--scaling strong` splits the 16,384 frames. `--impl reference`
 times the CPU oracle (the reference arm for this tier) instead.
 """
 from __future__ import annotations
@@ -36,7 +38,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--mode", default="shots", help="synthetic content: shots|uniform|constant|xgrad")
-    ap.add_argument("--frames", type=int, default=0, help="limit positions (debug; 0 = the whole config)")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="limit positions (debug; 0 = the whole config; per GPU under weak scaling)")
     ap.add_argument("--e2e-frames", type=int, default=512, help="positions per e2e step from pinned host memory")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline budget (oracle, rank 0, N=1)")
@@ -53,6 +56,9 @@ def parse():
     ap.add_argument("--bins", type=int, default=0, help="override the config's bins per channel (NEXT N4: 256)")
     ap.add_argument("--montage", type=int, default=0,
                     help="NEXT N1: time the two-job shot montage with this many tiles per canvas row (N = 1)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = each GPU processes one config's worth (the config's input N times over, "
+                         "sharded contiguously with halos); strong = the config itself split over N GPUs")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
                     help="f: sample -> hist -> [-1,0] (default); e: hist -> [-1,0] -> sample (NEXT N2, N = 1)")
     return ap.parse_args()
@@ -226,7 +232,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": wl.name, "frames_per_step": n, "bins": wl.bins, "ops": "hist+shotdiff"},
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -267,7 +273,7 @@ def run_graph_e(args):
     peak, peak_src = load_peaks()
     alg = job.R * (wl.frame_bytes + 3 * wl.bins * 4)
     line = {"metric": METRIC, "value": job.M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name + " graph e (hist -> [-1,0] -> sample)", "frames": job.M,
                        "required_frames": job.R, "bins": wl.bins, "ops": "hist(R)+diff_pairs"},
@@ -312,7 +318,7 @@ def run_montage(args):
         ts.append(a.elapsed_time(b))
     ms = statistics.median(ts)
     line = {"metric": METRIC, "value": M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name + " two-job shot montage (NEXT N1)", "frames": M,
                        "keyframes": int(len(pos)), "canvas": list(canvas.shape), "cols": args.montage,
@@ -387,7 +393,7 @@ def run_rounds(args):
     alg = M * (F + 3 * wl.bins * 4 + ds_b)
     ach = alg / (sum(hist_ms) / 1e3) / 1e9
     line = {"metric": METRIC, "value": M / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name, "frames": M, "rounds": len(round_ms), "round_frames": K,
                        "ops": "+".join(ops), "round_ms": round_ms,
@@ -422,11 +428,15 @@ def run_b200(args):
             dist.init_process_group(args.dist_backend)
 
     wl = scn_synth.WORKLOADS[args.config]
+    if args.scaling == "weak":
+        wl = wl.weak(world)  # per-GPU work fixed at one config as N grows
     if args.bins:
         import dataclasses
         wl = dataclasses.replace(wl, bins=args.bins)
     plan_ = scn_harness.plan(wl)
-    M = len(plan_[1]) if args.frames <= 0 else min(args.frames, len(plan_[1]))
+    # --frames limits one config's worth (per GPU under weak scaling)
+    lim = args.frames * (world if args.scaling == "weak" else 1)
+    M = len(plan_[1]) if args.frames <= 0 else min(lim, len(plan_[1]))
     plan_ = (plan_[0][:M], plan_[1][:M], plan_[2][:M])
     b, e = scn.scn_shard_range(M, world, rank)
     n = e - b
@@ -525,7 +535,7 @@ def run_b200(args):
     # ---- end-to-end through the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
-        ne = min(args.e2e_frames, M)
+        ne = min(args.e2e_frames * (world if args.scaling == "weak" else 1), M)
         eb, ee = scn.scn_shard_range(ne, world, rank)
         hj = scn_harness.HostJob(wl, eb, ee, with_halo=True, device=dev, plan_=plan_, staging_frames=48)
         ne_r = max(ee - eb, 1)
@@ -604,8 +614,8 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": M / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": wl.name, "frames": M, "width": wl.width, "height": wl.height, "bins": bins,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name, "frames": M, "frames_per_gpu": n, "width": wl.width, "height": wl.height, "bins": bins,
                        "sampling": str(wl.sampling[:2] if wl.sampling[0] != "range" else ("range", len(wl.sampling[1]), wl.sampling[2])),
                        "ops": "+".join(ops) + (f"+adaptive_cuts(W={cut_w})" if cut_w else "") +
                               (("+fused_peer_gather" if p2p else "+nccl_allgather") if world > 1 else ""),

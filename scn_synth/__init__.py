@@ -179,6 +179,21 @@ class Workload:
     def frame_bytes(self) -> int:
         return self.width * self.height * 3
 
+    def weak(self, g: int) -> "Workload":
+        """The config's input g times over, for weak scaling on g GPUs: one video grows to
+        g x its rows (a gather draws g x as many rows), several videos become g x as many
+        videos. Contiguous shards of the result hold exactly one config's worth each."""
+        import dataclasses
+        if g <= 1:
+            return self
+        if self.n_videos == 1:
+            smp = self.sampling
+            if smp[0] == "gather":
+                smp = (smp[0], smp[1], smp[2] * g)
+            return dataclasses.replace(self, name=f"{self.name} x{g} (weak)", rows_per_video=self.rows_per_video * g,
+                                       sampling=smp)
+        return dataclasses.replace(self, name=f"{self.name} x{g} (weak)", n_videos=self.n_videos * g)
+
 
 WORKLOADS = {
     "C1": Workload("C1-tiny-64x36-stride1-cuts", 64, 36, 1, 240, ("stride", 1), ("hist", "shotdiff"),
