@@ -333,18 +333,20 @@ __device__ __forceinline__ uint32_t win4(const uint32_t* w) {
   if constexpr ((I & 3) == 0) return w[I >> 2];
   else return __funnelshift_r(w[I >> 2], w[(I >> 2) + 1], 8 * (I & 3));
 }
+// The weights are 64, not 1: the result is (sum + 2) * 64 <= 65,408, so the output byte
+// (sum + 2) >> 2 sits exactly in bits 8-15 — no shift and no mask afterwards.
 template <int M>
-__device__ __forceinline__ uint32_t ds_sum(const uint32_t* t, const uint32_t* b) {  // sum + 2, <= 1022
+__device__ __forceinline__ uint32_t ds_sum(const uint32_t* t, const uint32_t* b) {  // (sum + 2) * 64
   constexpr int I = 2 * M - (M % 3);
-  return __dp4a(win4<I>(b), 0x01000001u, __dp4a(win4<I>(t), 0x01000001u, 2u));
+  return __dp4a(win4<I>(b), 0x40000040u, __dp4a(win4<I>(t), 0x40000040u, 128u));
 }
-// Packing: two 10-bit sums at 16-bit spacing (one IMAD), >> 2 and mask give two
-// output bytes at bytes 0 and 2; one PRMT interleaves the two halves.
+// Packing: two scaled sums at 16-bit spacing (one IMAD: no carry, each < 2^16) put output
+// bytes m and m+2 in bytes 1 and 3; one PRMT interleaves the two words' bytes 1 and 3.
 template <int Q>
 __device__ __forceinline__ uint32_t ds_word4(const uint32_t* t, const uint32_t* b) {
-  const uint32_t t02 = ((ds_sum<4 * Q + 2>(t, b) * 65536u + ds_sum<4 * Q>(t, b)) >> 2) & 0x00FF00FFu;
-  const uint32_t t13 = ((ds_sum<4 * Q + 3>(t, b) * 65536u + ds_sum<4 * Q + 1>(t, b)) >> 2) & 0x00FF00FFu;
-  return __byte_perm(t02, t13, 0x6240);
+  const uint32_t t02 = ds_sum<4 * Q + 2>(t, b) * 65536u + ds_sum<4 * Q>(t, b);
+  const uint32_t t13 = ds_sum<4 * Q + 3>(t, b) * 65536u + ds_sum<4 * Q + 1>(t, b);
+  return __byte_perm(t02, t13, 0x7351);
 }
 // Funnel-free variant (SCN_DS_VAR=2): a pair (X_i, X_{i+3}) that straddles words k, k+1
 // is summed by two dp4a on the aligned words with single-byte weights (FMA pipe only).
