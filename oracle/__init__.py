@@ -6,7 +6,7 @@ package. The product package ``paper_1805_07339_b200`` never imports it and
 shares no code with it (the only shared module is the input generator
 ``scn_synth``).
 
-Thin ctypes wrapper over ``liboracle_scn.so`` (plain single-threaded C,
+Thin ctypes wrapper over ``libscn_oracle.so`` (plain single-threaded C,
 ``oracle/scn_oracle.c``); every function there cites the PAPER.md passage it
 follows. Pins: ``tests/test_oracle_*.py``.
 """
