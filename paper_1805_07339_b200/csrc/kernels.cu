@@ -100,7 +100,12 @@ struct Layout {
   uint32_t table;
   uint32_t ring, stride;
   int stages;
+  uint32_t ring_hi = 0;  // split layout: slots n_lo.. live above the table
+  int n_lo = 0;
   __device__ __forceinline__ uint32_t slot(int s) const { return ring + (uint32_t)s * stride; }
+  __device__ __forceinline__ uint32_t slot_split(int s) const {
+    return s < n_lo ? ring + (uint32_t)s * stride : ring_hi + (uint32_t)(s - n_lo) * stride;
+  }
 };
 
 // Shared-memory layout: 1 KB control block at the bottom, the lane-private table at
@@ -119,6 +124,33 @@ __device__ __forceinline__ Layout make_layout(uint32_t base, uint32_t smem_bytes
   L.stages = L.table >= L.ring + need ? (int)((L.table - L.ring - need) / L.stride) + 1 : 0;
   if (L.stages > kMaxStages) L.stages = kMaxStages;
   if (L.table < base + kCtrlBytes) L.stages = 0;
+  return L;
+}
+
+// Split layout of the fused hist + downsample kernel at B = 16 (VAR bit 128): the
+// 64 KB PRMT block of channels 0/1 at the first 64 KB boundary above the control
+// block, channel 2's pair keys in 16 KB right below it as tab2[key][lane / 2] (64-byte
+// rows of 16 counters shared by lanes 2l, 2l+1), and ring slots both below tab2 and
+// above the block. Against the 96 KB table this frees 16 KB and the 64 KB alignment
+// waste, so 4K row-pair tiles get 3 stages instead of 2 (1080p: 8-row tiles instead of
+// 6). Lanes 2l and 2l+1 hit the same bank only when their channel-2 keys differ with
+// equal parity (a 2-way conflict); equal keys are one address (aggregated).
+constexpr uint32_t kTab2Bytes = 16384;
+constexpr uint32_t kSplitTab2 = kTab2Bytes;
+__device__ __forceinline__ Layout make_layout_split(uint32_t base, uint32_t smem_bytes, uint32_t tile) {
+  Layout L;
+  L.ctrl = base;
+  const uint32_t end = base + smem_bytes;
+  const uint32_t block = (base + kCtrlBytes + kTab2Bytes + 65535u) & ~65535u;
+  L.table = block - kTab2Bytes;
+  L.ring = (base + kCtrlBytes + 127) & ~127u;
+  L.stride = (tile + 127) & ~127u;
+  L.ring_hi = block + 65536u;
+  const int lo = L.table >= L.ring + tile ? (int)((L.table - L.ring - tile) / L.stride) + 1 : 0;
+  const int hi = end >= L.ring_hi + tile ? (int)((end - L.ring_hi - tile) / L.stride) + 1 : 0;
+  L.stages = lo + hi > kMaxStages ? kMaxStages : lo + hi;
+  L.n_lo = lo < L.stages ? lo : L.stages;
+  if (L.ring_hi > end) L.stages = 0;
   return L;
 }
 
@@ -185,8 +217,8 @@ __device__ __forceinline__ void pair_unit_all(const uint32_t* w, uint32_t lane4,
 // c * 128 is the ATOMS immediate); channel 2 keeps 128-byte rows, tab2[key][lane], in the
 // 32 KB after the block (table | key << 7 | lane << 2 + 64 KB: shift + LOP3). 16 of the
 // unit's 24 keys cost one instruction instead of two; the table is still 96 KB.
-template <int LOGB, int K_, int I, bool PRMT>
-__device__ __forceinline__ void wpair_key_step(uint32_t K, uint32_t lane4) {
+template <int LOGB, int K_, int I, bool PRMT, bool H2>
+__device__ __forceinline__ void wpair_key_step(uint32_t K, uint32_t lane4, uint32_t lane4h) {
   constexpr int J = 4 * K_ + I;  // byte of the first pixel of the pair
   constexpr int c = J % 3;
   constexpr int B = 1 << LOGB;
@@ -195,13 +227,21 @@ __device__ __forceinline__ void wpair_key_step(uint32_t K, uint32_t lane4) {
     red_shared_add_off<c * 128>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
     return;
   }
+  if constexpr (H2 && c == 2) {  // split layout: tab2 | key << 6 | (lane / 2) << 2
+    constexpr uint32_t kmask6 = ((1u << (2 * LOGB)) - 1u) << 6;
+    uint32_t x;
+    if constexpr (8 * I >= 6) x = K >> (8 * I - 6);
+    else x = K << (6 - 8 * I);
+    red_shared_add_off<0>(lop3_and_or<kmask6>(x, lane4h));
+    return;
+  }
   uint32_t x;
   if constexpr (8 * I >= 7) x = K >> (8 * I - 7);
   else x = K << (7 - 8 * I);
   red_shared_add_off<(PRMT ? 65536 : c * B * B * 128)>(lop3_and_or<kmask>(x, lane4));
 }
-template <int LOGB, int K_, bool PRMT>
-__device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
+template <int LOGB, int K_, bool PRMT, bool H2>
+__device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4, uint32_t lane4h) {
   constexpr uint32_t f = (1u << LOGB) - 1u;
   constexpr uint32_t M1 = f * 0x01010101u, M2 = (f << LOGB) * 0x01010101u;
   const uint32_t a = w[K_] >> (8 - LOGB);
@@ -213,19 +253,21 @@ __device__ __forceinline__ void wpair_word(const uint32_t* w, uint32_t lane4) {
   } else {
     Kw = (a & M1) | (b & M2);
   }
-  wpair_key_step<LOGB, K_, 0, PRMT>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 1, PRMT>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 2, PRMT>(Kw, lane4);
-  wpair_key_step<LOGB, K_, 3, PRMT>(Kw, lane4);
+  wpair_key_step<LOGB, K_, 0, PRMT, H2>(Kw, lane4, lane4h);
+  wpair_key_step<LOGB, K_, 1, PRMT, H2>(Kw, lane4, lane4h);
+  wpair_key_step<LOGB, K_, 2, PRMT, H2>(Kw, lane4, lane4h);
+  wpair_key_step<LOGB, K_, 3, PRMT, H2>(Kw, lane4, lane4h);
 }
 template <int LOGB, int VAR = 0>
-__device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4) {
+__device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4, uint32_t lane4h = 0) {
   if constexpr ((VAR & 8) || LOGB == 0) {  // adjacent-pixel pairing (previous default, SCN_HIST_VAR=8)
     pair_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 24>{});
   } else {
     constexpr bool P = LOGB == 4 && !(VAR & 64);  // B = 16: PRMT table layout (VAR bit 64: the previous one)
-    wpair_word<LOGB, 0, P>(w, lane4); wpair_word<LOGB, 1, P>(w, lane4); wpair_word<LOGB, 2, P>(w, lane4);
-    wpair_word<LOGB, 3, P>(w, lane4); wpair_word<LOGB, 4, P>(w, lane4); wpair_word<LOGB, 5, P>(w, lane4);
+    constexpr bool H = P && (VAR & 128);          // split layout: channel 2 in half-lane rows
+    wpair_word<LOGB, 0, P, H>(w, lane4, lane4h); wpair_word<LOGB, 1, P, H>(w, lane4, lane4h);
+    wpair_word<LOGB, 2, P, H>(w, lane4, lane4h); wpair_word<LOGB, 3, P, H>(w, lane4, lane4h);
+    wpair_word<LOGB, 4, P, H>(w, lane4, lane4h); wpair_word<LOGB, 5, P, H>(w, lane4, lane4h);
   }
 }
 
@@ -402,7 +444,13 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int BP = 1 << LOGB;
   const uint32_t base = smem_addr(smem);
-  const Layout L = make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align, p.stage_bytes);
+  constexpr bool kSplit = MODE == 2 && LOGB == 4 && (VAR & 128) && !(VAR & 64) && !(VAR & 32);
+  const Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.tile)
+                          : make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align, p.stage_bytes);
+  auto slot_of = [&](int s) -> uint32_t {
+    if constexpr (kSplit) return L.slot_split(s);
+    else return L.slot(s);
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
@@ -469,7 +517,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           const bool wrapped = t - t0 >= S;
           if (wrapped) store_next(s);  // tile t - S, released just now
           mbar_arrive_expect_tx(full0 + 8 * s, bytes);
-          tma_load_1d(L.slot(s), reinterpret_cast<const void*>(frame_addr(p.src, item) + off), bytes, full0 + 8 * s);
+          tma_load_1d(slot_of(s), reinterpret_cast<const void*>(frame_addr(p.src, item) + off), bytes, full0 + 8 * s);
           if (wrapped) {
             bulk_commit();
             bulk_wait_read<0>();
@@ -504,8 +552,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * s, bytes);
         const void* src = reinterpret_cast<const void*>(frame_addr(p.src, item) + off);
-        if (p.l2_hint) tma_load_1d_hint(L.slot(s), src, bytes, full0 + 8 * s, policy);  // frames are read once
-        else tma_load_1d(L.slot(s), src, bytes, full0 + 8 * s);
+        if (p.l2_hint) tma_load_1d_hint(slot_of(s), src, bytes, full0 + 8 * s, policy);  // frames are read once
+        else tma_load_1d(slot_of(s), src, bytes, full0 + 8 * s);
         if (++s == L.stages) { s = 0; ph ^= 1; }
       }
     }
@@ -514,7 +562,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
 
   // ---------------- consumers ----------------
   const int ctid = threadIdx.x;  // 0 .. kConsThreads-1
-  const uint32_t lane4 = L.table | ((uint32_t)lane << 2);
+  // split layout: channels 0/1 in the 64 KB block after tab2, channel 2 in tab2 (half lanes)
+  const uint32_t lane4 = (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
+  const uint32_t lane4h = L.table | ((uint32_t)lane >> 1 << 2);
   int s = 0;
   uint32_t ph = 0;
   uint32_t rot = 0;  // rotates unit->thread assignment across tiles so all warps share the work
@@ -553,17 +603,40 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const int rows = kSingle ? 3 * B : 3 * BP * BP;
     for (int r = ctid; r < rows; r += kConsThreads) {
       uint32_t ra = L.table + (uint32_t)r * 128u;
+      uint32_t sum = 0;
+      if constexpr (kSplit) {  // tab01[key][c] in the block after tab2; channel 2: tab2[key], 64-byte rows
+        const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
+        if (c < 2) {
+          ra = L.table + kTab2Bytes + key * 256u + c * 128u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t a = ra + (uint32_t)(((j + r) & 7) * 16);
+            const uint4 v = lds128(a);
+            sum += v.x + v.y + v.z + v.w;
+            sts128(a, make_uint4(0, 0, 0, 0));
+          }
+        } else {
+          ra = L.table + key * 64u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t a = ra + (uint32_t)(((j + r) & 3) * 16);
+            const uint4 v = lds128(a);
+            sum += v.x + v.y + v.z + v.w;
+            sts128(a, make_uint4(0, 0, 0, 0));
+          }
+        }
+      } else {
       if constexpr (kPrmtTable) {  // row (c, key): tab01[key][c] for c < 2, tab2[key] after the 64 KB block
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         ra = c < 2 ? L.table + key * 256u + c * 128u : L.table + 65536u + key * 128u;
       }
-      uint32_t sum = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t a = ra + (uint32_t)(((j + r) & 7) * 16);
         const uint4 v = lds128(a);
         sum += v.x + v.y + v.z + v.w;
         sts128(a, make_uint4(0, 0, 0, 0));
+      }
       }
       if (sum) {
         if (kSingle) {
@@ -623,7 +696,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     if constexpr (kTmaStore) {
       if (t - t0 >= L.stages) mbar_wait(sfree0 + 8 * s, ph ^ 1);  // the slot's previous output is stored
     }
-    const uint32_t slot = L.slot(s);
+    const uint32_t slot = slot_of(s);
     const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
     if constexpr (MODE == 2 || MODE == 3) {
@@ -646,8 +719,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         load_unit(a, wt);
         load_unit(a + rg.rowb, wb);
         if constexpr (MODE == 2) {
-          hist_unit_pair<LOGB, VAR & 64>(wt, lane4);
-          hist_unit_pair<LOGB, VAR & 64>(wb, lane4);
+          hist_unit_pair<LOGB, VAR & (64 | 128)>(wt, lane4, lane4h);
+          hist_unit_pair<LOGB, VAR & (64 | 128)>(wb, lane4, lane4h);
         }
         if (dsf) {
           ds_unit_v<(VAR & 16) ? 2 : ((VAR >> 2) & 1)>(wt, wb, o);
@@ -665,7 +738,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         for (uint32_t u = first; u < rg.upr; u += kConsThreads) {
           uint32_t w[12];
           load_unit(slot + (rows - 1) * rg.rowb + u * 48u, w);
-          hist_unit_pair<LOGB, VAR & 64>(w, lane4);
+          hist_unit_pair<LOGB, VAR & (64 | 128)>(w, lane4, lane4h);
         }
       }
       rot = (rot + npairs) % kConsThreads;
@@ -821,6 +894,7 @@ __global__ void __launch_bounds__(256) downsample_generic_kernel(FrameSrc src, i
 // ---------------------------------------------------------------------------
 static int g_num_sms = 0;
 static int g_smem_optin = 0;
+static int g_smem_reserved = 0;  // shared memory the system reserves per block (dynamic smem starts after it)
 
 static cudaError_t device_props() {
   if (g_num_sms) return cudaSuccess;
@@ -829,7 +903,9 @@ static cudaError_t device_props() {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  return cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  e = cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  return cudaDeviceGetAttribute(&g_smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
 }
 
 static int log2_exact(int b) {
@@ -888,6 +964,7 @@ static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused /
 static int g_tma_hint = 0;     // SCN_TMA_HINT=1: L2 evict_first policy on the frame loads
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
+static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
 static void read_tuning() {
   if (g_tune_warps >= 0) return;
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -909,6 +986,7 @@ static void read_tuning() {
   g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
   g_tma_hint = env_int("SCN_TMA_HINT", 0);
   g_ds_store = env_int("SCN_DS_STORE", 0);
+  g_fused_split = env_int("SCN_FUSED_SPLIT", 1);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
@@ -929,6 +1007,30 @@ static int rows_per_tile(int64_t rowb, uint32_t table_bytes, int stages, uint32_
   int r = (int)(ring / stages / cost) & ~1;
   if (r < 4) r = (int)(ring / 2 / cost) & ~1;
   return r;
+}
+
+// Rows per tile for the split layout (make_layout_split, mirrored here with the dynamic
+// smem base = the per-block reserved size): the largest even row count (tile <= 64 KB)
+// whose tiles give >= 3 ring stages over the two ring segments; 0 if none. The device
+// recomputes the same layout and traps on < 2 stages.
+static int rows_per_tile_split(int64_t rowb, uint32_t env_tile) {
+  const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin;
+  const uint32_t block = (base + kCtrlBytes + kSplitTab2 + 65535u) & ~65535u;
+  const uint32_t tab2 = block - kSplitTab2, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
+  if (hi > end) return 0;
+  auto stages = [&](int r) {
+    const uint32_t tile = (uint32_t)(r * rowb), stride = (tile + 127u) & ~127u;
+    const int lo = tab2 >= ring + tile ? (int)((tab2 - ring - tile) / stride) + 1 : 0;
+    const int up = end >= hi + tile ? (int)((end - hi - tile) / stride) + 1 : 0;
+    return lo + up;
+  };
+  if (env_tile) {
+    const int r = (int)((int64_t)env_tile / rowb) & ~1;
+    return r >= 2 && stages(r) >= 2 ? r : 0;
+  }
+  for (int r = (int)(65536 / rowb) & ~1; r >= 2; r -= 2)
+    if (stages(r) >= 3) return r;
+  return 0;
 }
 
 // TMA bulk stores of the downsample output need every output row segment 16-byte aligned:
@@ -1054,7 +1156,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   read_tuning();
   const int64_t pitch = j.ds_pitch > 0 ? j.ds_pitch : (int64_t)(j.width / 2) * 3;
   const bool tstore = lb == 4 && g_fused_warps == 8 && g_ds_var == 1 && ds_store_ok(j.width, pitch, j.ds_out);
-  int rpt = rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env, tstore);
+  // split layout (default at B = 16 with the 8-warp dp4a kernel): more ring for the same table
+  const int rsplit = (lb == 4 && !tstore && g_fused_split && g_fused_warps == 8 && g_ds_var == 1 && g_tune_var == 0)
+                         ? rows_per_tile_split(rowb, g_fused_tile_env) : 0;
+  int rpt = rsplit ? rsplit : rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env, tstore);
   if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
   const bool fused = lb >= 0 && j.width % 16 == 0 && rpt >= 2 && j.n_halo == 0;
   if (!fused) {
@@ -1083,6 +1188,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       if (tstore) {
         p.stage_bytes = (uint32_t)(rpt / 2) * (uint32_t)(j.width / 2) * 3u;
         return launch_tma<2, 4, 8, 4 | 32>(p, st);
+      }
+      if (rsplit) {
+        p.table_bytes = kSplitTab2 + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
+        return launch_tma<2, 4, 8, 4 | 128>(p, st);
       }
       if (g_fused_warps == 8 && g_ds_var == 2) return launch_tma<2, 4, 8, 16>(p, st);
       if (g_fused_warps == 8 && g_ds_var == 1 && g_tune_var == 64) return launch_tma<2, 4, 8, 4 | 64>(p, st);

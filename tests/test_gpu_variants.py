@@ -1,8 +1,9 @@
 """Every selectable kernel variant (env knobs) stays bit-exact: the
 north_star's per-warp match_any bins (K2a), one key per byte at B = 16, the previous
 adjacent-pixel pairing, the pre-PRMT table layout, the bytewise SWAR downsample, the LDG downsample kernel, the downsample output
-staged in the ring slot and written by the producer's TMA bulk stores, and
-non-default warp counts / tile sizes."""
+staged in the ring slot and written by the producer's TMA bulk stores, the fused
+kernel's previous 96 KB table layout (SCN_FUSED_SPLIT=0; the split layout is the
+default), and non-default warp counts / tile sizes."""
 import os
 import subprocess
 import sys
@@ -22,6 +23,8 @@ VARIANTS = [
     {"SCN_DS_VAR": "2"},
     {"SCN_DS_IMPL": "1"},
     {"SCN_DS_STORE": "1"},
+    {"SCN_FUSED_SPLIT": "0"},
+    {"SCN_FUSED_TILE": "23040"},
     {"SCN_HIST_WARPS": "8", "SCN_FUSED_WARPS": "16"},
     {"SCN_HIST_TILE": "15360", "SCN_FUSED_TILE": "23040", "SCN_DS_TILE": "64512"},
 ]
