@@ -567,7 +567,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   const uint32_t lane4h = L.table | ((uint32_t)lane >> 1 << 2);
   int s = 0;
   uint32_t ph = 0;
-  uint32_t rot = 0;  // rotates unit->thread assignment across tiles so all warps share the work
+  // Units are dealt round-robin over the consumer threads across tile boundaries: a thread's
+  // next unit (pair) index in the current tile is carried from the previous tile (minus
+  // that tile's unit count), so every warp shares the work and a tile costs no division.
+  uint32_t ucur = (uint32_t)ctid;
   int64_t cur = -1;
 
   auto out_row = [&](int64_t item) -> uint32_t* {
@@ -662,7 +665,6 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // row-pair tiling constants of the downsample modes (unused otherwise)
   struct {
     uint32_t rowb, upr, dq, dr, last_rows, in_bytes, ow3s;
-    float inv_upr;
     int64_t pitch, ow3, tile_out;
     uint8_t* ds_frame;
   } rg{};
@@ -672,17 +674,23 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     rg.dq = (uint32_t)kConsThreads / rg.upr;
     rg.dr = (uint32_t)kConsThreads - rg.dq * rg.upr;
     rg.last_rows = (uint32_t)(p.height - (p.tpf - 1) * p.rows_per_tile);
-    rg.inv_upr = 1.0f / (float)rg.upr;
     rg.pitch = p.ds_pitch;
     rg.ow3 = (int64_t)(p.width / 2) * 3;
     rg.tile_out = (int64_t)(p.rows_per_tile / 2) * rg.pitch;
     rg.in_bytes = (p.tile + 127u) & ~127u;
     rg.ow3s = (uint32_t)rg.ow3;
   }
+  // MODE 2/3: the carried unit pair as (row pair, column unit), ucur = rpc * upr + xcc
+  uint32_t rpc = 0, xcc = 0;
+  if constexpr (MODE == 2 || MODE == 3) {
+    rpc = (uint32_t)ctid / rg.upr;
+    xcc = (uint32_t)ctid - rpc * rg.upr;
+  }
   int64_t item = t0 / p.tpf;
   int32_t k = (int32_t)(t0 - item * p.tpf);
-  for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
-    if (item != cur) {
+  const int32_t ntiles = (int32_t)(t1 - t0);  // < 2^31 tiles per CTA
+  for (int32_t i = 0; i < ntiles; ++i, (++k == p.tpf) ? (k = 0, ++item) : 0) {
+    if (k == 0 || i == 0) {  // a new frame (item changes exactly when k wraps)
       if (cur >= 0) flush(cur);
       cur = item;
       if constexpr (MODE == 2 || MODE == 3) {
@@ -694,10 +702,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     const uint32_t len = (uint32_t)((uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile);
     mbar_wait(full0 + 8 * s, ph);
     if constexpr (kTmaStore) {
-      if (t - t0 >= L.stages) mbar_wait(sfree0 + 8 * s, ph ^ 1);  // the slot's previous output is stored
+      if (i >= L.stages) mbar_wait(sfree0 + 8 * s, ph ^ 1);  // the slot's previous output is stored
     }
     const uint32_t slot = slot_of(s);
-    const uint32_t first = (uint32_t)ctid >= rot ? (uint32_t)ctid - rot : (uint32_t)ctid + kConsThreads - rot;
 
     if constexpr (MODE == 2 || MODE == 3) {
       // fused: rows [k*R, k*R + rows) of the frame; unit pairs over row pairs.
@@ -706,14 +713,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       const uint32_t rows = (k == p.tpf - 1) ? rg.last_rows : (uint32_t)p.rows_per_tile;
       const uint32_t npairs = (rows / 2) * rg.upr;
       uint8_t* dsf = (item >= p.n_halo) ? rg.ds_frame + (int64_t)k * rg.tile_out : nullptr;
-      // unit pair u -> (row pair rp, column unit xc): first / upr by a float reciprocal with an
-      // exact correction, then advanced incrementally (no per-unit division)
-      uint32_t rp = __float2uint_rz(__uint2float_rz(first) * rg.inv_upr);
-      if ((rp + 1) * rg.upr <= first) ++rp;
-      if (rp * rg.upr > first) --rp;
-      uint32_t xc = first - rp * rg.upr;
-      for (uint32_t u = first; u < npairs;
-           u += kConsThreads, rp += rg.dq, xc += rg.dr, (xc >= rg.upr) ? (xc -= rg.upr, ++rp) : 0) {
+      // unit pair u -> (row pair rp, column unit xc), carried from the previous tile and
+      // advanced incrementally (no division)
+      uint32_t u = ucur, rp = rpc, xc = xcc;
+      for (; u < npairs; u += kConsThreads, rp += rg.dq, xc += rg.dr, (xc >= rg.upr) ? (xc -= rg.upr, ++rp) : 0) {
         const uint32_t a = slot + rp * 2u * rg.rowb + xc * 48u;
         uint32_t wt[12], wb[12], o[6];
         load_unit(a, wt);
@@ -734,17 +737,20 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           }
         }
       }
+      ucur = u - npairs;  // same column unit, rows / 2 row pairs earlier in the next tile
+      rpc = rp - rows / 2;
+      xcc = xc;
       if (MODE == 2 && (rows & 1)) {  // odd last row of an odd-height frame: histogram only
-        for (uint32_t u = first; u < rg.upr; u += kConsThreads) {
+        for (uint32_t v = (uint32_t)ctid; v < rg.upr; v += kConsThreads) {
           uint32_t w[12];
-          load_unit(slot + (rows - 1) * rg.rowb + u * 48u, w);
+          load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
           hist_unit_pair<LOGB, VAR & (64 | 128)>(w, lane4, lane4h);
         }
       }
-      rot = (rot + npairs) % kConsThreads;
     } else {
       const uint32_t nunits = len / 48u;
-      for (uint32_t u = first; u < nunits; u += kConsThreads) {
+      uint32_t u = ucur;
+      for (; u < nunits; u += kConsThreads) {
         uint32_t w[12];
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == 0) {
@@ -783,7 +789,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         const uint32_t bin = (v * (uint32_t)B) >> 8;
         emit(item, (int)((j % 3) * B + bin), 1u);
       }
-      rot = (rot + nunits) % kConsThreads;
+      ucur = u - nunits;
     }
     if constexpr (kTmaStore) fence_proxy_async_smem();  // staged output visible to the bulk store
     __syncwarp();
