@@ -626,7 +626,7 @@ def run_b200(args):
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("hist_tma_kernel<2,4,8,4> (scn_run_hist_downsample incl. memset)" if do_ds else
+                         "kernel": ("hist_tma_kernel<2,4,8,132> split layout (scn_run_hist_downsample incl. memset)" if do_ds else
                                     "hist_tma_kernel<0,4,16,0> + shotdiff_kernel (scn_run_hist_shotdiff incl. "
                                     "memset)" if do_diff else "hist_tma_kernel<0,4,16,0> (scn_run_histogram)"),
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": hist_ms_max,

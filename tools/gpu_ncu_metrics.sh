@@ -3,7 +3,7 @@
 # hist (C2, 2048 frames), fused hist+ds (C4, 1024 frames), ds-only (C4, 1024 frames).
 # Summarised by tools/ncu_summarize.py into gpurun_out/ncu_counters_*.json.
 mkdir -p gpurun_out
-make -j8 all > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+[ -f paper_1805_07339_b200/libscn.so ] || make -j8 all > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,\
 sm__cycles_elapsed.avg,sm__cycles_elapsed.avg.per_second,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,\
 smsp__inst_executed_op_shared_atom.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum,\
