@@ -1163,7 +1163,8 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   const int64_t pitch = j.ds_pitch > 0 ? j.ds_pitch : (int64_t)(j.width / 2) * 3;
   const bool tstore = lb == 4 && g_fused_warps == 8 && g_ds_var == 1 && ds_store_ok(j.width, pitch, j.ds_out);
   // split layout (default at B = 16 with the 8-warp dp4a kernel): more ring for the same table
-  const int rsplit = (lb == 4 && !tstore && g_fused_split && g_fused_warps == 8 && g_ds_var == 1 && g_tune_var == 0)
+  const int rsplit = (lb == 4 && !tstore && g_fused_split && g_ds_var == 1 && g_tune_var == 0 &&
+                      (g_fused_warps == 8 || g_fused_warps == 12 || g_fused_warps == 16))
                          ? rows_per_tile_split(rowb, g_fused_tile_env) : 0;
   int rpt = rsplit ? rsplit : rows_per_tile(rowb, 3u * 256u * 128u, 3, g_fused_tile_env, tstore);
   if (rpt > j.height) rpt = j.height + (j.height & 1);  // whole frame in one tile
@@ -1197,6 +1198,8 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       }
       if (rsplit) {
         p.table_bytes = kSplitTab2 + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
+        if (g_fused_warps == 12) return launch_tma<2, 4, 12, 4 | 128>(p, st);
+        if (g_fused_warps == 16) return launch_tma<2, 4, 16, 4 | 128>(p, st);
         return launch_tma<2, 4, 8, 4 | 128>(p, st);
       }
       if (g_fused_warps == 8 && g_ds_var == 2) return launch_tma<2, 4, 8, 16>(p, st);
