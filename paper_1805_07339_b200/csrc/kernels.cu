@@ -30,7 +30,10 @@
 // K2f hist_tma_kernel<2, LOGB>: K1+K2 with the 2x box downsample fused into the
 //   consumer (a thread takes the two vertically adjacent 48-byte units of a
 //   row pair, histograms both and emits 8 output pixels), so each sampled
-//   frame is read from HBM once (reading Q12).
+//   frame is read from HBM once (reading Q12). At B = 16 (VAR bit 128, default)
+//   it uses the split layout (make_layout_split): channel 2's pair keys in 16 KB
+//   of half-lane rows and ring slots on both sides of the 64 KB PRMT block, so
+//   1080p and 4K both get 3 stages of 46 KB row-pair tiles.
 // K3 shotdiff_kernel: one warp per position, L1 over 3*B counters with
 //   __reduce_add_sync.
 // K4 hist_tma_kernel<3, 4>: the same ring without the table (downsample only);
