@@ -277,12 +277,24 @@ __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4
 // Single-key lane-private counting for B = 2^LOGB in [32, 256] (NEXT N4): byte J of
 // channel J % 3 -> tab[c][bin][lane], bin = top LOGB bits; table 32 KB-aligned per
 // channel for B = 256 so the address is table | bin << 7 | lane << 2 (one LOP3).
-template <int LOGB, int J>
+// B = 256 PRMT layout (kPrmt256, default): channels 0 and 1 share 256-byte rows of a
+// 64 KB-aligned block, tab01[bin][c][lane], so ONE PRMT drops the byte (its bin) into
+// byte 1 of the address (c * 128 is the ATOMS immediate); channel 2 keeps 128-byte rows
+// in the 32 KB after the block (PRMT + IMAD as before). 2/3 of the bytes cost one
+// instruction instead of two; the table is still 96 KB.
+template <int LOGB, int J, bool P256>
 __device__ __forceinline__ void single_unit_step(const uint32_t* w, uint32_t lane4) {
   constexpr int c = J % 3;
   constexpr int B = 1 << LOGB;
   uint32_t addr;
-  if constexpr (LOGB == 8) {
+  if constexpr (P256 && c < 2) {
+    red_shared_add_off<c * 128>(__byte_perm(w[J >> 2], lane4, 0x7604u | ((J & 3) << 4)));
+    return;
+  } else if constexpr (P256) {
+    addr = __byte_perm(w[J >> 2], 0u, 0x4440u + (J & 3)) * 128u + lane4;
+    red_shared_add_off<65536>(addr);
+    return;
+  } else if constexpr (LOGB == 8) {
     // B = 256: the key is the byte; PRMT zero-extends it (ALU), IMAD scales and adds the
     // lane offset (FMA pipe): one op on each pipe instead of two ALU ops
     addr = __byte_perm(w[J >> 2], 0u, 0x4440u + (J & 3)) * 128u + lane4;
@@ -291,13 +303,13 @@ __device__ __forceinline__ void single_unit_step(const uint32_t* w, uint32_t lan
   }
   red_shared_add_off<c * B * 128>(addr);
 }
-template <int LOGB, int... J>
+template <int LOGB, bool P256, int... J>
 __device__ __forceinline__ void single_unit_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, J...>) {
-  (single_unit_step<LOGB, J>(w, lane4), ...);
+  (single_unit_step<LOGB, J, P256>(w, lane4), ...);
 }
-template <int LOGB>
+template <int LOGB, bool P256 = false>
 __device__ __forceinline__ void hist_unit_single(const uint32_t* w, uint32_t lane4) {
-  single_unit_all<LOGB>(w, lane4, std::make_integer_sequence<int, 48>{});
+  single_unit_all<LOGB, P256>(w, lane4, std::make_integer_sequence<int, 48>{});
 }
 
 __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   const int B = (MODE == 1) ? p.bins : BP;
   constexpr bool kSingle = (MODE == 1 || MODE == 4);  // one key per byte: flush rows are (c, bin) directly
+  constexpr bool kPrmt256 = MODE == 4 && LOGB == 8 && !(VAR & 64);  // B = 256 PRMT table layout
   // B = 16 pair keys with word-parallel pairing: the PRMT table layout (see wpair_key_step)
   constexpr bool kPrmtTable = (MODE == 0 || MODE == 2) && LOGB == 4 && !(VAR & 8) && !(VAR & 64);
   constexpr bool kTmaStore = (MODE == 2 || MODE == 3) && (VAR & 32);  // downsample out via TMA bulk stores
@@ -632,7 +645,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           }
         }
       } else {
-      if constexpr (kPrmtTable) {  // row (c, key): tab01[key][c] for c < 2, tab2[key] after the 64 KB block
+      if constexpr (kPrmtTable || kPrmt256) {  // row (c, key): tab01[key][c] for c < 2, tab2[key] after the block
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         ra = c < 2 ? L.table + key * 256u + c * 128u : L.table + 65536u + key * 128u;
       }
@@ -772,7 +785,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             if ((peers & lt) == 0) atomicAdd(wb + key, (uint32_t)__popc(peers));
           }
         } else if constexpr (MODE == 4) {
-          hist_unit_single<LOGB>(w, lane4);
+          hist_unit_single<LOGB, kPrmt256>(w, lane4);
         } else {
           const uint32_t Bu = (uint32_t)B;
 #pragma unroll
@@ -1118,7 +1131,10 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       case 32: return launch_tma<4, 5>(p, st);
       case 64: return launch_tma<4, 6>(p, st);
       case 128: return launch_tma<4, 7>(p, st);
-      default: return launch_tma<4, 8>(p, st);
+      default:
+        if (g_tune_var == 64) return launch_tma<4, 8, 16, 64>(p, st);  // previous shifted-key layout (A/B)
+        p.table_align = 65536u;  // the PRMT layout's 64 KB block
+        return launch_tma<4, 8>(p, st);
     }
   }
   p.table_bytes = 3u * (uint32_t)j.bins * 128u;
