@@ -49,6 +49,9 @@ def main():
     check(w1, ("hist", "shotdiff", "downsample"), 16, host=True)
     check(w1, ("hist", "shotdiff"), 256)   # NEXT N4 (single shifted key, B = 256)
     check(w1, ("hist", "shotdiff"), 64)
+    # fused split layout with several row-pair tiles per frame (24-row tiles, 4-row tail)
+    w3 = Workload("san3", 640, 100, 1, 6, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 4})
+    check(w3, ("hist", "downsample"), 16)
     next_rows()
     print("sanitize_run ok")
 
