@@ -46,9 +46,11 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <utility>
 
 namespace scn {
@@ -918,16 +920,26 @@ static int g_num_sms = 0;
 static int g_smem_optin = 0;
 static int g_smem_reserved = 0;  // shared memory the system reserves per block (dynamic smem starts after it)
 
+// Queried once per process (all GPUs of a B200 box are identical) and published together:
+// concurrent first calls from several host threads serialize on the mutex, and a failed
+// query (e.g. no device yet) is retried by the next call.
+static std::mutex g_props_mu;
+static std::atomic<bool> g_props_ok{false};
 static cudaError_t device_props() {
-  if (g_num_sms) return cudaSuccess;
-  int dev = 0;
+  if (g_props_ok.load(std::memory_order_acquire)) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(g_props_mu);
+  if (g_props_ok.load(std::memory_order_relaxed)) return cudaSuccess;
+  int dev = 0, sms = 0, optin = 0, reserved = 0;
   cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
   if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e != cudaSuccess) return e;
-  return cudaDeviceGetAttribute(&g_smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  g_num_sms = sms;
+  g_smem_optin = optin;
+  g_smem_reserved = reserved;
+  g_props_ok.store(true, std::memory_order_release);
+  return cudaSuccess;
 }
 
 static int log2_exact(int b) {
@@ -987,8 +999,8 @@ static int g_tma_hint = 0;     // SCN_TMA_HINT=1: L2 evict_first policy on the f
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
-static void read_tuning() {
-  if (g_tune_warps >= 0) return;
+static std::once_flag g_tuning_once;
+static void read_tuning_once() {
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
   int t = env_int("SCN_HIST_TILE", (int)kTile);
   if (t < 48 || t % 48 != 0 || t > 65536) t = (int)kTile;
@@ -1014,6 +1026,7 @@ static void read_tuning() {
     g_hist_match = impl && strcmp(impl, "match") == 0;
   }
 }
+static void read_tuning() { std::call_once(g_tuning_once, read_tuning_once); }
 
 // Rows per row-pair tile (measured): the largest even row count whose tiles
 // give `stages` ring stages next to a table of table_bytes, unless that is under 4 rows, in
