@@ -47,3 +47,16 @@ def test_graph_capture_replay(ops):
             assert (out["ds"].cpu().numpy()[:M] == DS).all()
     del g
     job.close()
+
+
+def test_concurrent_first_use_from_threads():
+    # fresh process: the one-time init (device properties, env tuning, smem opt-in) races
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for _ in range(3):
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "helpers", "threads_check.py")],
+                           capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        assert "threads_check ok" in r.stdout
