@@ -126,15 +126,15 @@ class ClockSampler:
 
 
 def traffic_from_profile(frames: int, F: int, kernel: str = "hist"):
-    """dram bytes per launch from the committed ncu --set full summary (bytes/frame x frames), or None."""
-    p = os.path.join(ROOT, "profiles", f"ncu_{kernel}_summary.json")
-    if not os.path.exists(p):
-        return None, None
-    d = json.load(open(p))
-    bpf = d.get("dram_bytes_per_frame")
-    if not bpf or d.get("frame_bytes") != F or d.get("kernel") != kernel:
-        return None, None
-    return float(bpf) * frames, d.get("source", p)
+    """dram bytes per launch from a committed ncu --set full summary of this kernel at this
+    frame size (profiles/ncu_<kernel>[_<tag>]_summary.json; bytes/frame x frames), or None."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{kernel}*_summary.json"))):
+        d = json.load(open(p))
+        bpf = d.get("dram_bytes_per_frame")
+        if bpf and d.get("frame_bytes") == F and d.get("kernel") == kernel:
+            return float(bpf) * frames, d.get("source", p)
+    return None, None
 
 
 # ---------------------------------------------------------------------------
