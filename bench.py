@@ -634,6 +634,8 @@ def run_b200(args):
                          # also against the nominal ~8 TB/s, and the second roofline
                          # (shared-atomic throughput of K2) next to its K0-measured capacity
                          "peak_nominal": NOMINAL_HBM_GBPS, "frac_nominal": achieved / NOMINAL_HBM_GBPS,
+                         # the measured stream ceiling for this kernel's read:write mix on a B200
+                         **stream_ceiling(do_ds, achieved),
                          "shared_atomics": atomic_roofline(bins, (e - jb + halo) * F, hist_ms_max, clk)},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -653,6 +655,20 @@ def run_b200(args):
 
 NOMINAL_HBM_GBPS = 8000.0  # B200 nominal HBM3e bandwidth (the north_star's "roughly 8 TB/s")
 K0_ATOMS_ILP = 31.8  # conflict-free lane-private red.shared lane-ops / SM-clock (profiles/r01_k0_micro_v2.json)
+
+
+# Measured HBM stream ceilings on a B200 (no compute): best TMA bulk read ring
+# (profiles/r01_k0_micro_v2.json, tma_read_t16384_s6_w17) and TMA bulk load + bulk store
+# at 4:1 read:write (profiles/r01_mix_ceiling.json, tma_r4w1_s4) — the mix of the fused
+# hist + downsample kernel (F read, F/4 written per frame).
+READ_CEILING_GBPS = 7565.8
+R4W1_CEILING_GBPS = 7140.5
+
+
+def stream_ceiling(do_ds, achieved):
+    c, src = ((R4W1_CEILING_GBPS, "profiles/r01_mix_ceiling.json tma_r4w1_s4 (TMA load + store, 4:1)") if do_ds else
+              (READ_CEILING_GBPS, "profiles/r01_k0_micro_v2.json tma_read_t16384_s6_w17 (TMA read ring)"))
+    return {"stream_ceiling": c, "frac_stream_ceiling": achieved / c, "stream_ceiling_source": src}
 
 
 def atomic_roofline(bins, in_bytes, ms, clk):
