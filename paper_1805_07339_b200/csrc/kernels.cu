@@ -84,6 +84,7 @@ struct HistParams {
   uint32_t table_align;
   uint32_t stage_bytes;  // VAR bit 32: per-slot staging of the tile's downsample output (after its input bytes)
   int32_t l2_hint;  // 1: TMA loads carry an L2 evict_first policy (SCN_TMA_HINT)
+  int32_t l2_prefetch;  // > 0: the producer bulk-prefetches tile t + l2_prefetch into L2 (SCN_L2_PREFETCH)
   int32_t n_dest;   // > 0: results go to every dest[g] (fused all-gather over peer memory)
   uint64_t dest[kMaxDest];
 };
@@ -563,10 +564,23 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       int64_t item = t0 / p.tpf;
       int32_t k = (int32_t)(t0 - item * p.tpf);
       const uint64_t policy = l2_policy_evict_first();
+      // L2 prefetch cursor, l2_prefetch tiles ahead of the load cursor
+      int64_t pitem = item;
+      int32_t pk = k;
+      for (int32_t i = 0; i < p.l2_prefetch; ++i)
+        if (++pk == p.tpf) { pk = 0; ++pitem; }
       for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
         const uint64_t off = (uint64_t)k * p.tile;
         const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
         const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
+        if (p.l2_prefetch > 0) {
+          if (t + p.l2_prefetch < t1) {
+            const uint64_t poff = (uint64_t)pk * p.tile;
+            const uint64_t plen = (uint64_t)p.F - poff < p.tile ? (uint64_t)p.F - poff : p.tile;
+            tma_prefetch_l2(reinterpret_cast<const void*>(frame_addr(p.src, pitem) + poff), (uint32_t)((plen + 15) & ~15ull));
+          }
+          if (++pk == p.tpf) { pk = 0; ++pitem; }
+        }
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * s, bytes);
         const void* src = reinterpret_cast<const void*>(frame_addr(p.src, item) + off);
@@ -996,6 +1010,7 @@ static int g_ds_impl = 0;   // SCN_DS_IMPL: 0 = TMA ring (MODE 3), 1 = LDG kerne
 static int g_hist_single = 0;  // SCN_HIST_SINGLE: B = 16 with one key per byte instead of pair keys
 static int g_fused_warps = 8;  // SCN_FUSED_WARPS: consumer warps of the fused / ds-only kernels (measured best: 8)
 static int g_tma_hint = 0;     // SCN_TMA_HINT=1: L2 evict_first policy on the frame loads
+static int g_l2_prefetch = -1;  // SCN_L2_PREFETCH=P: bulk L2 prefetch P tiles ahead (default: fused 1, else 0)
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
@@ -1019,6 +1034,7 @@ static void read_tuning_once() {
   g_hist_single = env_int("SCN_HIST_SINGLE", 0);
   g_fused_warps = env_int("SCN_FUSED_WARPS", 8);
   g_tma_hint = env_int("SCN_TMA_HINT", 0);
+  g_l2_prefetch = env_int("SCN_L2_PREFETCH", -1);
   g_ds_store = env_int("SCN_DS_STORE", 0);
   g_fused_split = env_int("SCN_FUSED_SPLIT", 1);
   {
@@ -1092,6 +1108,7 @@ static HistParams base_params(const HistJob& j) {
   p.smem_bytes = (uint32_t)g_smem_optin;
   read_tuning();
   p.l2_hint = g_tma_hint;
+  p.l2_prefetch = g_l2_prefetch > 0 ? g_l2_prefetch : 0;
   p.n_dest = j.n_dest;
   for (int g = 0; g < kMaxDest; ++g) p.dest[g] = j.dest[g];
   return p;
@@ -1210,6 +1227,9 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
     return launch_downsample(src, j.n_items, j.width, j.height, j.ds_out, st, launches, j.ds_pitch, j.ds_cols);
   }
   HistParams p = base_params(j);
+  // one tile of L2 bulk prefetch ahead of the ring (measured: C4 +0.8 %, C5 +1.7 %; it
+  // slows the read-only histogram kernel, which keeps 0)
+  p.l2_prefetch = g_l2_prefetch >= 0 ? g_l2_prefetch : 1;
   p.rows_per_tile = rpt;
   p.tile = (uint32_t)(rpt * rowb);
   p.tpf = (j.height + rpt - 1) / rpt;

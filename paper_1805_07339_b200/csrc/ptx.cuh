@@ -44,6 +44,10 @@ __device__ __forceinline__ void tma_load_1d_hint(uint32_t dst, const void* src, 
       "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
+// global -> L2 bulk prefetch (no shared memory, no completion tracking); bytes a multiple of 16
+__device__ __forceinline__ void tma_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

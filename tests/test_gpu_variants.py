@@ -24,6 +24,8 @@ VARIANTS = [
     {"SCN_DS_IMPL": "1"},
     {"SCN_DS_STORE": "1"},
     {"SCN_FUSED_SPLIT": "0"},
+    {"SCN_L2_PREFETCH": "0"},
+    {"SCN_L2_PREFETCH": "3"},
     {"SCN_FUSED_TILE": "23040"},
     {"SCN_HIST_WARPS": "8", "SCN_FUSED_WARPS": "16"},
     {"SCN_HIST_TILE": "15360", "SCN_FUSED_TILE": "23040", "SCN_DS_TILE": "64512"},
