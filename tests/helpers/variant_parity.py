@@ -37,6 +37,21 @@ def main():
                 if "downsample" in ops:
                     assert (out["ds"].cpu().numpy()[:M] == DS).all(), (wl.name, mode, ops)
             job.close()
+    # N4 bin counts (the B = 256 / 64 kernels have their own layouts and knobs)
+    for bins in (256, 64):
+        for wl in cases[1:]:
+            for mode in ("shots", "uniform"):
+                spec = wl.spec(mode=mode)
+                pl = scn_harness.plan(wl)
+                M = len(pl[1])
+                H, D, _ = oracle.run(spec, pl[0], pl[1], pl[2], 0, M, bins)
+                job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, spec=spec, plan_=pl)
+                out = job.alloc_outputs(("hist", "shotdiff"), bins)
+                job.run(out, ("hist", "shotdiff"), bins)
+                torch.cuda.synchronize()
+                assert (out["hist"].cpu().numpy().view(np.uint32)[:M] == H).all(), (wl.name, mode, bins)
+                assert (out["diff"].cpu().numpy().view(np.uint32)[:M] == D).all(), (wl.name, mode, bins)
+                job.close()
     print("variant_parity ok", {k: v for k, v in os.environ.items() if k.startswith("SCN_")})
 
 
