@@ -165,18 +165,6 @@ __device__ __forceinline__ void red_shared_add_off(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
 }
 
-// Bits [8-LOGB, 8) of byte J of the unit (the bin of that byte for B = 2^LOGB),
-// moved to bit DST of the result.
-template <int J, int DST, int LOGB>
-__device__ __forceinline__ uint32_t bin_field(const uint32_t* w) {
-  constexpr int src = 8 * (J & 3) + 8 - LOGB;
-  const uint32_t x = w[J >> 2];
-  uint32_t y;
-  if constexpr (src >= DST) y = x >> (src - DST);
-  else y = x << (DST - src);
-  return y & (((1u << LOGB) - 1u) << DST);
-}
-
 // Byte J of the unit shifted so its top LOGB bits (its bin) land at bit DST (unmasked).
 template <int J, int DST, int LOGB>
 __device__ __forceinline__ uint32_t bin_shift(const uint32_t* w) {
@@ -323,40 +311,8 @@ __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {
 }
 
 // ---- 2x box downsample of a 2 x 48-byte unit pair -> 24 output bytes --------
-// O = (a+b+c+d+2)>>2 computed bytewise without carries as
-//   (a>>2)+(b>>2)+(c>>2)+(d>>2) + (((a&3)+(b&3)+(c&3)+(d&3)+2)>>2)
-// which is exact (each term fits in its byte: 4*63+3 <= 255, 4*3+2 <= 255).
-template <int I>
-__device__ __forceinline__ uint32_t byte_of(const uint32_t* w) {
-  return (w[I >> 2] >> (8 * (I & 3))) & 0xFFu;
-}
-// output byte m (0..23) of the 8-pixel group: left source byte 2m - (m % 3), right = left + 3
-template <int M>
-struct DsIdx { static constexpr int L = 2 * M - (M % 3); static constexpr int R = L + 3; };
-
-template <int Q>
-__device__ __forceinline__ uint32_t ds_word(const uint32_t* t, const uint32_t* b) {
-  constexpr int m0 = 4 * Q, m1 = 4 * Q + 1, m2 = 4 * Q + 2, m3 = 4 * Q + 3;
-  const uint32_t TL = byte_of<DsIdx<m0>::L>(t) | byte_of<DsIdx<m1>::L>(t) << 8 | byte_of<DsIdx<m2>::L>(t) << 16 |
-                      byte_of<DsIdx<m3>::L>(t) << 24;
-  const uint32_t TR = byte_of<DsIdx<m0>::R>(t) | byte_of<DsIdx<m1>::R>(t) << 8 | byte_of<DsIdx<m2>::R>(t) << 16 |
-                      byte_of<DsIdx<m3>::R>(t) << 24;
-  const uint32_t BL = byte_of<DsIdx<m0>::L>(b) | byte_of<DsIdx<m1>::L>(b) << 8 | byte_of<DsIdx<m2>::L>(b) << 16 |
-                      byte_of<DsIdx<m3>::L>(b) << 24;
-  const uint32_t BR = byte_of<DsIdx<m0>::R>(b) | byte_of<DsIdx<m1>::R>(b) << 8 | byte_of<DsIdx<m2>::R>(b) << 16 |
-                      byte_of<DsIdx<m3>::R>(b) << 24;
-  const uint32_t hi = ((TL >> 2) & 0x3F3F3F3Fu) + ((TR >> 2) & 0x3F3F3F3Fu) + ((BL >> 2) & 0x3F3F3F3Fu) +
-                      ((BR >> 2) & 0x3F3F3F3Fu);
-  const uint32_t lo = (TL & 0x03030303u) + (TR & 0x03030303u) + (BL & 0x03030303u) + (BR & 0x03030303u) +
-                      0x02020202u;
-  return hi + ((lo >> 2) & 0x03030303u);
-}
-// Reference formulation (kept for readability; ds_unit below is the fast path).
-__device__ __forceinline__ void ds_unit_bytewise(const uint32_t* t, const uint32_t* b, uint32_t* o) {
-  o[0] = ds_word<0>(t, b); o[1] = ds_word<1>(t, b); o[2] = ds_word<2>(t, b);
-  o[3] = ds_word<3>(t, b); o[4] = ds_word<4>(t, b); o[5] = ds_word<5>(t, b);
-}
-
+// O = (a+b+c+d+2)>>2 per channel byte; output byte m of the 8-pixel group averages source
+// bytes i = 2m - (m % 3) and i + 3 of both rows.
 // Fast 2x2 average of 16 pixels x 2 rows (t, b: 12 words each) -> 8 pixels (6 words).
 // Per word: vertical partial sums of the high 6 bits (hv) and low 2 bits (lv) of
 // each byte; a funnel shift by 3 bytes aligns pixel 2x+1 over pixel 2x, so
