@@ -535,67 +535,26 @@ def run_b200(args):
     # ---- end-to-end through the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
-        ne = min(args.e2e_frames * (world if args.scaling == "weak" else 1), M)
-        eb, ee = scn.scn_shard_range(ne, world, rank)
-        hj = scn_harness.HostJob(wl, eb, ee, with_halo=True, device=dev, plan_=plan_, staging_frames=48)
-        ne_r = max(ee - eb, 1)
-        eo = {"hist": torch.empty((ne_r, 3, bins), dtype=torch.int32, device=dev),
-              "diff": torch.empty(ne_r, dtype=torch.int32, device=dev),
-              "scratch": torch.empty(3 * bins, dtype=torch.int32, device=dev)}
-        if do_ds:
-            eo["ds"] = torch.empty((ne_r, wl.height // 2, wl.width // 2, 3), dtype=torch.uint8, device=dev)
-        h_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in eo.items()
-                 if k == "hist" or (k == "diff" and do_diff) or (k == "ds" and do_ds)}
-        cs = torch.cuda.Stream(dev)
-
-        def e2e_step():
-            hj.run(eo, ops, bins, stream=stream, copy_stream=cs)
-            for k, hv in h_out.items():
-                hv.copy_(eo[k], non_blocking=True)
-
-        for _ in range(max(args.warmup, 1)):
-            e2e_step()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        ksteps = max(1, min(args.steps, 5))
-        e0.record(stream)
-        for _ in range(ksteps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_ms = float(te[0]) / ksteps
-        e2e = {"value": ne / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int((ee - eb) * wl.frame_bytes),
-               "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in h_out.values())),
-               "positions_per_step": ne, "ms_per_step": e2e_ms,
-               "h2d_GBps": (ee - eb) * wl.frame_bytes / (e2e_ms / 1e3) / 1e9,
-               "h2d_ceiling_note": "raw pinned H2D on the GPU box measured 55.4-55.6 GB/s (profiles/r01_h2d_ceiling.json)",
-               "path": "scn_run_pipeline_host: pinned host frames -> double-buffered H2D (copy stream) -> "
-                       "hist+shotdiff kernels -> D2H of hist+diff"}
-        hj.close()
+        e2e = run_e2e(args, wl, plan_, M, world, rank, dev, stream, ops, bins, do_diff, do_ds)
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nfr = 16
-        frames = np.empty((nfr, wl.height, wl.width, 3), dtype=np.uint8)
-        src = job.buf[: nfr * job.F16].view(nfr, job.F16)[:, : job.F].cpu().numpy()
-        frames[:] = src.reshape(nfr, wl.height, wl.width, 3)
-        n1, t1s = time_oracle(frames, bins, max(2.0, args.cpu_seconds / 3))
-        threads = os.cpu_count() or 1
-        ndone, tused = time_oracle_all_cores(frames, bins, args.cpu_seconds, threads)
-        cpu = {"value": ndone / tused, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "single_core_value": n1 / t1s,
-               "sample": f"positions {b}..{b + nfr - 1} of {args.config} ({wl.width}x{wl.height}), frames "
-                         f"pre-generated (untimed); {threads} independent instances of the single-threaded C "
-                         f"oracle over disjoint frames, {ndone} frames in {tused:.1f} s wall; one instance alone "
-                         f"{n1 / t1s:.1f} frames/s"}
+        try:
+            nfr = 16
+            # the oracle's input comes from the host generator (scn_synth), never from the GPU
+            frames = host_frames(wl, list(range(b, b + nfr)), plan_)
+            n1, t1s = time_oracle(frames, bins, max(2.0, args.cpu_seconds / 3))
+            threads = os.cpu_count() or 1
+            ndone, tused = time_oracle_all_cores(frames, bins, args.cpu_seconds, threads)
+            cpu = {"value": ndone / tused, "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "single_core_value": n1 / t1s,
+                   "sample": f"positions {b}..{b + nfr - 1} of {args.config} ({wl.width}x{wl.height}), frames "
+                             f"generated on the host (untimed); {threads} independent instances of the "
+                             f"single-threaded C oracle over disjoint frames, {ndone} frames in {tused:.1f} s wall; "
+                             f"one instance alone {n1 / t1s:.1f} frames/s"}
+        except Exception as ex:  # noqa: BLE001 (reported in the JSON line, the GPU numbers still print)
+            cpu = {"value": None, "kind": "oracle", "error": f"{type(ex).__name__}: {ex}"[:300]}
 
     if world > 1:
         dist.barrier()
@@ -651,6 +610,85 @@ def run_b200(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_e2e(args, wl, plan_, M, world, rank, dev, stream, ops, bins, do_diff, do_ds):
+    """The same metric end to end through scn_run_pipeline_host: each step copies its frames
+    from pinned host memory (H2D inside the timed region) and reads the result columns back
+    (D2H). A failure on any rank (e.g. pinned-memory exhaustion on an unfamiliar box) is
+    reported in the line instead of aborting the run; every rank still joins each
+    collective, so a local failure cannot hang the others."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_07339_b200 as scn
+    import scn_harness
+
+    def agree(ok: bool) -> bool:  # all ranks succeeded?
+        if world == 1:
+            return ok
+        f = torch.tensor([0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+        return float(f[0]) == 0.0
+
+    ne = min(args.e2e_frames * (world if args.scaling == "weak" else 1), M)
+    eb, ee = scn.scn_shard_range(ne, world, rank)
+    err, hj = None, None
+    try:
+        hj = scn_harness.HostJob(wl, eb, ee, with_halo=True, device=dev, plan_=plan_, staging_frames=48)
+        ne_r = max(ee - eb, 1)
+        eo = {"hist": torch.empty((ne_r, 3, bins), dtype=torch.int32, device=dev),
+              "diff": torch.empty(ne_r, dtype=torch.int32, device=dev),
+              "scratch": torch.empty(3 * bins, dtype=torch.int32, device=dev)}
+        if do_ds:
+            eo["ds"] = torch.empty((ne_r, wl.height // 2, wl.width // 2, 3), dtype=torch.uint8, device=dev)
+        h_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in eo.items()
+                 if k == "hist" or (k == "diff" and do_diff) or (k == "ds" and do_ds)}
+        cs = torch.cuda.Stream(dev)
+
+        def e2e_step():
+            hj.run(eo, ops, bins, stream=stream, copy_stream=cs)
+            for k, hv in h_out.items():
+                hv.copy_(eo[k], non_blocking=True)
+
+        for _ in range(max(args.warmup, 1)):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+    except Exception as ex:  # noqa: BLE001 (reported in the JSON line)
+        err = f"{type(ex).__name__}: {ex}"[:300]
+    if not agree(err is None):
+        if hj is not None:
+            hj.close()
+        return {"value": None, "unit": UNIT, "error": err or "failed on another rank"}
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ksteps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(ksteps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    d2h_r = sum(v.numel() * v.element_size() for v in h_out.values())
+    te = torch.tensor([e0.elapsed_time(e1), float(d2h_r)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = te.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(te, op=dist.ReduceOp.SUM)
+        te[0] = tmax[0]
+    hj.close()
+    e2e_ms = float(te[0]) / ksteps
+    h2d = ne * wl.frame_bytes  # whole job: every rank's frames (each rank copies its shard)
+    return {"value": ne / (e2e_ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(te[1]),
+            "positions_per_step": ne, "ms_per_step": e2e_ms,
+            "h2d_GBps": h2d / (e2e_ms / 1e3) / 1e9,
+            "h2d_ceiling_note": "raw pinned H2D on the GPU box measured 55.4-55.6 GB/s per GPU "
+                                "(profiles/r01_h2d_ceiling.json)",
+            "path": "scn_run_pipeline_host: pinned host frames -> double-buffered H2D (copy stream) -> "
+                    "hist+shotdiff kernels -> D2H of the result columns"}
+
 
 
 NOMINAL_HBM_GBPS = 8000.0  # B200 nominal HBM3e bandwidth (the north_star's "roughly 8 TB/s")
