@@ -227,7 +227,7 @@ def run_reference(args):
             one_step(pool)
         dt = time.perf_counter() - t0
     fps = n * args.steps / dt
-    sample = (f"positions 0..{n - 1} of {args.config} ({wl.width}x{wl.height}) per step, frames pre-generated "
+    sample = (f"positions 0..{n - 1} of {args.config} ({wl.width}x{wl.height}) per step, frames generated on the host "
               f"(untimed), split over {threads} independent instances of the single-threaded C oracle")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
