@@ -575,6 +575,17 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     }
   };
 
+  // Flush without zeroing (default): the lane-private counters keep accumulating over the
+  // CTA's frames and a frame's count of a row is its 32-lane sum minus the sum at the
+  // previous flush (exact mod 2^32). Each thread always flushes the same rows
+  // (r = ctid + i * kConsThreads), so the previous sums live in registers and the flush
+  // reads the table without writing it back (half the shared-memory traffic).
+  // VAR bit 256: the previous flush that re-zeroes every row (A/B).
+  constexpr bool kZeroFlush = (VAR & 256) != 0;
+  constexpr int kSnapN = (768 + kConsThreads - 1) / kConsThreads;  // rows <= 3 * 256
+  uint32_t snap[kSnapN];
+#pragma unroll
+  for (int i = 0; i < kSnapN; ++i) snap[i] = 0;
   auto flush = [&](int64_t item) {
     if constexpr (MODE == 3) return;
     named_bar(kBarId, kConsThreads);
@@ -592,7 +603,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       return;
     }
     const int rows = kSingle ? 3 * B : 3 * BP * BP;
-    for (int r = ctid; r < rows; r += kConsThreads) {
+#pragma unroll
+    for (int i = 0; i < kSnapN; ++i) {
+      const int r = ctid + i * kConsThreads;
+      if (r >= rows) break;
       uint32_t ra = L.table + (uint32_t)r * 128u;
       uint32_t sum = 0;
       if constexpr (kSplit) {  // tab01[key][c] in the block after tab2; channel 2: tab2[key], 64-byte rows
@@ -604,7 +618,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             const uint32_t a = ra + (uint32_t)(((j + r) & 7) * 16);
             const uint4 v = lds128(a);
             sum += v.x + v.y + v.z + v.w;
-            sts128(a, make_uint4(0, 0, 0, 0));
+            if constexpr (kZeroFlush) sts128(a, make_uint4(0, 0, 0, 0));
           }
         } else {
           ra = L.table + key * 64u;
@@ -613,7 +627,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             const uint32_t a = ra + (uint32_t)(((j + r) & 3) * 16);
             const uint4 v = lds128(a);
             sum += v.x + v.y + v.z + v.w;
-            sts128(a, make_uint4(0, 0, 0, 0));
+            if constexpr (kZeroFlush) sts128(a, make_uint4(0, 0, 0, 0));
           }
         }
       } else {
@@ -626,8 +640,13 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         const uint32_t a = ra + (uint32_t)(((j + r) & 7) * 16);
         const uint4 v = lds128(a);
         sum += v.x + v.y + v.z + v.w;
-        sts128(a, make_uint4(0, 0, 0, 0));
+        if constexpr (kZeroFlush) sts128(a, make_uint4(0, 0, 0, 0));
       }
+      }
+      if constexpr (!kZeroFlush) {  // this frame's count = the row sum since the previous flush
+        const uint32_t total = sum;
+        sum = total - snap[i];
+        snap[i] = total;
       }
       if (sum) {
         if (kSingle) {
@@ -970,6 +989,7 @@ static int g_l2_prefetch = -1;  // SCN_L2_PREFETCH=P: bulk L2 prefetch P tiles a
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
+static int g_flush_zero = 0;   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
 static std::once_flag g_tuning_once;
 static void read_tuning_once() {
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -993,6 +1013,7 @@ static void read_tuning_once() {
   g_l2_prefetch = env_int("SCN_L2_PREFETCH", -1);
   g_ds_store = env_int("SCN_DS_STORE", 0);
   g_fused_split = env_int("SCN_FUSED_SPLIT", 1);
+  g_flush_zero = env_int("SCN_FLUSH_ZERO", 0);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
@@ -1107,6 +1128,7 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
         if (g_tune_var == 64) return launch_tma<0, 4, 16, 64>(p, st);  // previous table layout (A/B)
         if (g_tune_warps == 12) return launch_tma<0, 4, 12>(p, st);
         if (g_tune_warps == 8) return launch_tma<0, 4, 8>(p, st);
+        if (g_flush_zero) return launch_tma<0, 4, 16, 256>(p, st);
         return launch_tma<0, 4>(p, st);
     }
   }
@@ -1206,6 +1228,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       }
       if (rsplit) {
         p.table_bytes = kSplitTab2 + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
+        if (g_flush_zero && g_fused_warps == 8) return launch_tma<2, 4, 8, 4 | 128 | 256>(p, st);
         if (g_fused_warps == 12) return launch_tma<2, 4, 12, 4 | 128>(p, st);
         if (g_fused_warps == 16) return launch_tma<2, 4, 16, 4 | 128>(p, st);
         return launch_tma<2, 4, 8, 4 | 128>(p, st);

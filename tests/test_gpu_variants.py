@@ -24,6 +24,7 @@ VARIANTS = [
     {"SCN_DS_IMPL": "1"},
     {"SCN_DS_STORE": "1"},
     {"SCN_FUSED_SPLIT": "0"},
+    {"SCN_FLUSH_ZERO": "1"},
     {"SCN_L2_PREFETCH": "0"},
     {"SCN_L2_PREFETCH": "3"},
     {"SCN_FUSED_TILE": "23040"},
