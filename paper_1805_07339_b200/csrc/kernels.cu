@@ -525,10 +525,19 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       int32_t pk = k;
       for (int32_t i = 0; i < p.l2_prefetch; ++i)
         if (++pk == p.tpf) { pk = 0; ++pitem; }
+      // the frame's address is loaded (sparse tables: a global read of the row pointer) once
+      // per frame and BEFORE the empty-slot wait, so its latency overlaps the wait instead of
+      // delaying the copy once the slot frees
+      int64_t base_item = -1;
+      uint64_t base = 0;
       for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
         const uint64_t off = (uint64_t)k * p.tile;
         const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
         const uint32_t bytes = (uint32_t)((len + 15) & ~15ull);
+        if (item != base_item) {
+          base_item = item;
+          base = frame_addr(p.src, item);
+        }
         if (p.l2_prefetch > 0) {
           if (t + p.l2_prefetch < t1) {
             const uint64_t poff = (uint64_t)pk * p.tile;
@@ -537,9 +546,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           }
           if (++pk == p.tpf) { pk = 0; ++pitem; }
         }
+        const void* src = reinterpret_cast<const void*>(base + off);
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * s, bytes);
-        const void* src = reinterpret_cast<const void*>(frame_addr(p.src, item) + off);
         if (p.l2_hint) tma_load_1d_hint(slot_of(s), src, bytes, full0 + 8 * s, policy);  // frames are read once
         else tma_load_1d(slot_of(s), src, bytes, full0 + 8 * s);
         if (++s == L.stages) { s = 0; ph ^= 1; }
