@@ -85,6 +85,7 @@ struct HistParams {
   uint32_t stage_bytes;  // VAR bit 32: per-slot staging of the tile's downsample output (after its input bytes)
   int32_t l2_hint;  // 1: TMA loads carry an L2 evict_first policy (SCN_TMA_HINT)
   int32_t l2_prefetch;  // > 0: the producer bulk-prefetches tile t + l2_prefetch into L2 (SCN_L2_PREFETCH)
+  int32_t max_stages;   // > 0: cap on the ring depth (SCN_MAX_STAGES)
   int32_t n_dest;   // > 0: results go to every dest[g] (fused all-gather over peer memory)
   uint64_t dest[kMaxDest];
 };
@@ -419,8 +420,12 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr int BP = 1 << LOGB;
   const uint32_t base = smem_addr(smem);
   constexpr bool kSplit = MODE == 2 && LOGB == 4 && (VAR & 128) && !(VAR & 64) && !(VAR & 32);
-  const Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.tile)
-                          : make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align, p.stage_bytes);
+  Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.tile)
+                    : make_layout(base, p.smem_bytes, p.tile, p.table_bytes, p.table_align, p.stage_bytes);
+  if (p.max_stages > 0 && L.stages > p.max_stages) {  // ring-depth cap (SCN_MAX_STAGES, measurement knob)
+    L.stages = p.max_stages;
+    if (L.n_lo > L.stages) L.n_lo = L.stages;
+  }
   auto slot_of = [&](int s) -> uint32_t {
     if constexpr (kSplit) return L.slot_split(s);
     else return L.slot(s);
@@ -998,7 +1003,8 @@ static int g_l2_prefetch = -1;  // SCN_L2_PREFETCH=P: bulk L2 prefetch P tiles a
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
-static int g_flush_zero = 0;   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
+static int g_flush_zero = 0;
+static int g_max_stages = 0;   // SCN_MAX_STAGES=S: cap the ring depth (measurement knob)   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
 static std::once_flag g_tuning_once;
 static void read_tuning_once() {
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -1023,6 +1029,7 @@ static void read_tuning_once() {
   g_ds_store = env_int("SCN_DS_STORE", 0);
   g_fused_split = env_int("SCN_FUSED_SPLIT", 1);
   g_flush_zero = env_int("SCN_FLUSH_ZERO", 0);
+  g_max_stages = env_int("SCN_MAX_STAGES", 0);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
@@ -1095,6 +1102,7 @@ static HistParams base_params(const HistJob& j) {
   read_tuning();
   p.l2_hint = g_tma_hint;
   p.l2_prefetch = g_l2_prefetch > 0 ? g_l2_prefetch : 0;
+  p.max_stages = g_max_stages >= 2 ? g_max_stages : 0;
   p.n_dest = j.n_dest;
   for (int g = 0; g < kMaxDest; ++g) p.dest[g] = j.dest[g];
   return p;
@@ -1276,6 +1284,10 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   p.total_tiles = n * p.tpf;
   p.table_bytes = 0;
   p.table_align = 128;
+  // three stages, not as many as fit: a deeper ring streams slower (measured: C4 6.76 ->
+  // 6.89, C5 6.76 -> 6.94 TB/s with 3 instead of 4 stages; pure TMA reads likewise,
+  // profiles/r01_read_order_micro.json)
+  if (!p.max_stages) p.max_stages = 3;
   if (tstore) {
     p.stage_bytes = (uint32_t)(rpt / 2) * (uint32_t)(width / 2) * 3u;
     return launch_tma<3, 4, 8, 4 | 32>(p, st);

@@ -25,6 +25,7 @@ VARIANTS = [
     {"SCN_DS_STORE": "1"},
     {"SCN_FUSED_SPLIT": "0"},
     {"SCN_FLUSH_ZERO": "1"},
+    {"SCN_MAX_STAGES": "2"},
     {"SCN_L2_PREFETCH": "0"},
     {"SCN_L2_PREFETCH": "3"},
     {"SCN_FUSED_TILE": "23040"},
