@@ -1004,7 +1004,7 @@ static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
 static int g_flush_zero = 0;
-static int g_max_stages = 0;   // SCN_MAX_STAGES=S: cap the ring depth (measurement knob)   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
+static int g_max_stages = 0;   // SCN_MAX_STAGES=S: ring-depth cap (default 3; measurement knob)   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
 static std::once_flag g_tuning_once;
 static void read_tuning_once() {
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -1102,7 +1102,10 @@ static HistParams base_params(const HistJob& j) {
   read_tuning();
   p.l2_hint = g_tma_hint;
   p.l2_prefetch = g_l2_prefetch > 0 ? g_l2_prefetch : 0;
-  p.max_stages = g_max_stages >= 2 ? g_max_stages : 0;
+  // at most three ring stages: deeper rings stream slower on B200 (pure TMA reads, the
+  // downsample-only kernel, and the kernels whose smaller tables leave room for 4-8 stages:
+  // bins 8 / 32 / 64 / 128 run +5-9 % with 3; profiles/r01_tune.jsonl, SCN_MAX_STAGES A/B)
+  p.max_stages = g_max_stages >= 2 ? g_max_stages : 3;
   p.n_dest = j.n_dest;
   for (int g = 0; g < kMaxDest; ++g) p.dest[g] = j.dest[g];
   return p;
@@ -1284,10 +1287,6 @@ static cudaError_t launch_ds_tma(const FrameSrc& src, int64_t n, int32_t width, 
   p.total_tiles = n * p.tpf;
   p.table_bytes = 0;
   p.table_align = 128;
-  // three stages, not as many as fit: a deeper ring streams slower (measured: C4 6.76 ->
-  // 6.89, C5 6.76 -> 6.94 TB/s with 3 instead of 4 stages; pure TMA reads likewise,
-  // profiles/r01_read_order_micro.json)
-  if (!p.max_stages) p.max_stages = 3;
   if (tstore) {
     p.stage_bytes = (uint32_t)(rpt / 2) * (uint32_t)(width / 2) * 3u;
     return launch_tma<3, 4, 8, 4 | 32>(p, st);
