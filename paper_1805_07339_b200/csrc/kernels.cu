@@ -922,6 +922,7 @@ __global__ void __launch_bounds__(256) downsample_generic_kernel(FrameSrc src, i
 static int g_num_sms = 0;
 static int g_smem_optin = 0;
 static int g_smem_reserved = 0;  // shared memory the system reserves per block (dynamic smem starts after it)
+static int g_grid_cap = 0;       // SCN_GRID=G: persistent CTAs (default: one per SM; measurement knob)
 
 // Queried once per process (all GPUs of a B200 box are identical) and published together:
 // concurrent first calls from several host threads serialize on the mutex, and a failed
@@ -971,6 +972,7 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
   }
   int grid = g_num_sms;
+  if (g_grid_cap > 0 && g_grid_cap < grid) grid = g_grid_cap;  // SCN_GRID (measurement knob)
   if (p.total_tiles < grid) grid = (int)p.total_tiles;
   if (grid < 1) return cudaSuccess;
   fn<<<grid, NW * 32 + 32, p.smem_bytes, st>>>(p);
@@ -1003,8 +1005,8 @@ static int g_l2_prefetch = -1;  // SCN_L2_PREFETCH=P: bulk L2 prefetch P tiles a
 static int g_hist_match = 0;   // SCN_HIST_IMPL=match: the north_star's per-warp bins + __match_any_sync (K2a)
 static int g_ds_store = 0;     // SCN_DS_STORE=1: downsample output by producer TMA bulk stores (measured slower)
 static int g_fused_split = 1;  // SCN_FUSED_SPLIT=0: the fused kernel's previous 96 KB table layout
-static int g_flush_zero = 0;
-static int g_max_stages = 0;   // SCN_MAX_STAGES=S: ring-depth cap (default 3; measurement knob)   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
+static int g_flush_zero = 0;   // SCN_FLUSH_ZERO=1: the previous flush that re-zeroes the table (A/B)
+static int g_max_stages = 0;   // SCN_MAX_STAGES=S: ring-depth cap (default 3; measurement knob)
 static std::once_flag g_tuning_once;
 static void read_tuning_once() {
   g_tune_warps = env_int("SCN_HIST_WARPS", kDefaultConsWarps);
@@ -1030,6 +1032,7 @@ static void read_tuning_once() {
   g_fused_split = env_int("SCN_FUSED_SPLIT", 1);
   g_flush_zero = env_int("SCN_FLUSH_ZERO", 0);
   g_max_stages = env_int("SCN_MAX_STAGES", 0);
+  g_grid_cap = env_int("SCN_GRID", 0);
   {
     const char* impl = getenv("SCN_HIST_IMPL");
     g_hist_match = impl && strcmp(impl, "match") == 0;
