@@ -11,6 +11,7 @@ CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra -shared
 PKG       := paper_1805_07339_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libscn.so
+LIB_TUNE  := $(PKG)/libscn_tuning.so
 LIB_SRCS  := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
 LIB_HDRS  := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/scn.h
 
@@ -25,12 +26,18 @@ CUDA_HOME  ?= /usr/local/cuda
 all: $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(DEMO)
 
 lib: $(LIB)
+# measurement build: the same kernels with the SCN_* environment knobs (grid, tiles,
+# ring depth, L2 prefetch) read once per process; loaded by the binding when SCN_LIB=tuning
+tuning: $(LIB_TUNE)
 oracle: $(ORACLE) $(SYNTH_HOST)
 micro: $(MICRO)
 
 # .git/logs/HEAD changes with every commit, so the embedded SHA (scn_version) stays current
 $(LIB): $(LIB_SRCS) $(LIB_HDRS) $(wildcard .git/logs/HEAD)
 	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_GIT_SHA=\"$(GIT_SHA)\" -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+
+$(LIB_TUNE): $(LIB_SRCS) $(LIB_HDRS) $(wildcard .git/logs/HEAD)
+	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_TUNING -DSCN_GIT_SHA=\"$(GIT_SHA)-tuning\" $(LIB_SRCS) -o $@
 
 $(SYNTH_HOST): scn_synth/synth_host.c scn_synth/scn_synth.h
 	$(CC) $(CFLAGS) $< -o $@
@@ -50,6 +57,6 @@ $(MICRO): tools/micro/k0.cu
 	$(NVCC) $(ARCH) -O3 -o $@ $<
 
 clean:
-	rm -f $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(MICRO) $(DEMO)
+	rm -f $(LIB) $(LIB_TUNE) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(MICRO) $(DEMO)
 
-.PHONY: all lib oracle micro clean
+.PHONY: all lib tuning oracle micro clean

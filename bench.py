@@ -5,10 +5,12 @@ Contract (driver): `python bench.py --gpus N --steps K --warmup W` (torchrun for
 N > 1) prints ONE JSON line on rank 0. A step is one pass of the whole hot path
 (sample -> per-channel histogram -> [-1,0] shot-diff, + NCCL all-gather of the
 result columns when N > 1) over the BASELINE config C2 (1920x1080 RGB8,
-16,384 frames, Stride 1), frames already resident in HBM. Weak scaling by default:
-at N GPUs the film is N x 16,384 frames, split contiguously (each GPU one config's
-worth + its recomputed 1-frame halo); `--scaling strong` splits the 16,384 frames. `--impl reference`
-times the CPU oracle (the reference arm for this tier) instead.
+16,384 frames, Stride 1), frames already resident in HBM, captured once per rank
+as a CUDA graph and replayed. Strong scaling by default: at N GPUs the 16,384
+frames are split contiguously (2,048 per GPU at N = 8, each shard with its
+recomputed 1-frame halo, BASELINE "frames sharded with 1-frame halo");
+`--scaling weak` runs the config N times over instead. `--impl reference` times
+the CPU oracle (the reference arm for this tier) instead.
 """
 from __future__ import annotations
 
@@ -40,7 +42,7 @@ def parse():
     ap.add_argument("--mode", default="shots", help="synthetic content: shots|uniform|constant|xgrad")
     ap.add_argument("--frames", type=int, default=0,
                     help="limit positions (debug; 0 = the whole config; per GPU under weak scaling)")
-    ap.add_argument("--e2e-frames", type=int, default=512, help="positions per e2e step from pinned host memory")
+    ap.add_argument("--e2e-frames", type=int, default=1024, help="positions per e2e step from pinned host memory")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline budget (oracle, rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -56,9 +58,14 @@ def parse():
     ap.add_argument("--bins", type=int, default=0, help="override the config's bins per channel (NEXT N4: 256)")
     ap.add_argument("--montage", type=int, default=0,
                     help="NEXT N1: time the two-job shot montage with this many tiles per canvas row (N = 1)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = each GPU processes one config's worth (the config's input N times over, "
-                         "sharded contiguously with halos); strong = the config itself split over N GPUs")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong (default) = the config itself split contiguously over N GPUs (BASELINE C2: "
+                         "16,384 frames sharded with 1-frame halo); weak = each GPU processes one config's worth "
+                         "(the config's input N times over)")
+    ap.add_argument("--shape", default="", help="override the config's frame size, WxH (e.g. 1366x768)")
+    ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--hist-impl", type=int, default=0,
+                    help="scn_set_hist_impl: 0 lane-private pair keys (default), 1 K2a match per byte, 2 K2a' packed")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
                     help="f: sample -> hist -> [-1,0] (default); e: hist -> [-1,0] -> sample (NEXT N2, N = 1)")
     return ap.parse_args()
@@ -125,15 +132,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profile(frames: int, F: int, kernel: str = "hist"):
+def traffic_from_profile(frames: int, F: int, kernel: str, lib_version: str):
     """dram bytes per launch from a committed ncu --set full summary of this kernel at this
-    frame size (profiles/ncu_<kernel>[_<tag>]_summary.json; bytes/frame x frames), or None."""
+    frame size (profiles/ncu_<kernel>[_<tag>]_summary.json; bytes/frame x frames), the
+    summary's source, and whether the capture's git SHA is the library's (scn_version)."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{kernel}*_summary.json"))):
         d = json.load(open(p))
         bpf = d.get("dram_bytes_per_frame")
         if bpf and d.get("frame_bytes") == F and d.get("kernel") == kernel:
-            return float(bpf) * frames, d.get("source", p)
+            sha = d.get("git_sha")
+            match = bool(sha) and sha[:12] in lib_version
+            if not match:
+                print(f"warning: {os.path.basename(p)} was captured at {sha} but the library is {lib_version}",
+                      file=sys.stderr)
+            return float(bpf) * frames, {"source": d.get("source", p), "summary": os.path.relpath(p, ROOT),
+                                         "capture_sha": sha, "matches_library": match}
     return None, None
 
 
@@ -405,6 +419,16 @@ def run_rounds(args):
     return 0
 
 
+def _apply_shape(wl, args):
+    import dataclasses
+    if args.bins:
+        wl = dataclasses.replace(wl, bins=args.bins)
+    if args.shape:
+        w, h = (int(x) for x in args.shape.lower().split("x"))
+        wl = dataclasses.replace(wl, name=f"{wl.name} @{w}x{h}", width=w, height=h)
+    return wl
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -423,16 +447,18 @@ def run_b200(args):
     dev = torch.device("cuda", dev_index)
     if world > 1:
         if args.dist_backend == "nccl":
+            # NCCL's INIT log names the communicator size ("nranks N"), so a run's rank count is checkable
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
+    scn.scn_set_hist_impl(args.hist_impl)
 
     wl = scn_synth.WORKLOADS[args.config]
     if args.scaling == "weak":
         wl = wl.weak(world)  # per-GPU work fixed at one config as N grows
-    if args.bins:
-        import dataclasses
-        wl = dataclasses.replace(wl, bins=args.bins)
+    wl = _apply_shape(wl, args)
     plan_ = scn_harness.plan(wl)
     # --frames limits one config's worth (per GPU under weak scaling)
     lim = args.frames * (world if args.scaling == "weak" else 1)
@@ -441,7 +467,10 @@ def run_b200(args):
     b, e = scn.scn_shard_range(M, world, rank)
     n = e - b
     bins = wl.bins
-    stream = torch.cuda.current_stream(dev)
+    # one non-default stream for everything (CUDA graphs cannot capture the legacy stream);
+    # made current so torch's collectives and graph replays are ordered on it too
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     cut_w = args.cuts
     jb = b
     if cut_w > 0:  # NEXT N3: the shard starts W positions early (warmup), computed and discarded
@@ -455,24 +484,35 @@ def run_b200(args):
     ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
     out = job.alloc_outputs(ops, bins)
     p2p = world > 1 and args.gather == "p2p"
+    gather_note = None
     if p2p and (do_ds or cut_w or not do_diff):
         raise SystemExit("--gather p2p covers the hist + shot-diff step only")
-    gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 and not p2p else None
-    peer = scn_harness.PeerColumns(M, bins, dist, dev) if p2p else None
-
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    peer = None
+    if p2p:  # the fused peer-memory gather, or NCCL if any rank cannot map its peers' columns
+        err = None
+        try:
+            peer = scn_harness.PeerColumns(M, bins, dist, dev)
+        except Exception as ex:  # noqa: BLE001 (reported in the JSON line)
+            err = f"{type(ex).__name__}: {ex}"[:200]
+        bad = torch.tensor([0.0 if err is None else 1.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if float(bad[0]):
+            if peer is not None:
+                peer.close()
+            peer, p2p = None, False
+            gather_note = "p2p unavailable, fell back to NCCL all_gather: " + (err or "failed on another rank")
+    gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 and peer is None else None
+    if gather is not None and jb == b:  # the kernels write straight into the all-gather's send block
+        out["hist"] = gather.hist
+        if do_diff:
+            out["diff"] = gather.diff
     launches = [0]
 
-    def step(k=None):
-        if k is not None:
-            ev[k][0].record(stream)
+    def compute():
         if peer is not None:  # HIST + shot-diff writing this rank's rows into every rank's columns
             scn.scn_run_hist_shotdiff_to(job.seq, b, e, bins, peer.hist_ptrs, peer.diff_ptrs, rank, out["scratch"],
                                          stream)
             launches[0] += scn.scn_last_launch_count()
-            if k is not None:
-                ev[k][1].record(stream)
-                ev[k][2].record(stream)
             return
         if do_ds:  # HIST + 2x downsample in one read of each frame (reading Q12)
             scn.scn_run_hist_downsample(job.seq, jb, e, bins, out["hist"], out["ds"], stream)
@@ -486,51 +526,82 @@ def run_b200(args):
         else:
             scn.scn_run_histogram(job.seq, jb, e, bins, out["hist"], stream)
             launches[0] += scn.scn_last_launch_count()
-        if k is not None:
-            ev[k][1].record(stream)
         if cut_w > 0:
             scn.scn_run_adaptive_cuts(job.seq, b, e, cut_w, out["diff"], 4, 1, wl.width * wl.height // 8, d_cut,
                                       stream)
             launches[0] += scn.scn_last_launch_count()
+
+    def exchange():
         if gather is not None:
             gather.gather(out["hist"][b - jb:], out["diff"][b - jb:] if do_diff else None, n)
-        if k is not None:
-            ev[k][2].record(stream)
+
+    def step():
+        compute()
+        exchange()
 
     for _ in range(max(args.warmup, 0)):
         step()
+    torch.cuda.synchronize(dev)
+    # One CUDA graph per rank for the step (memset + histogram + shot-diff + all-gather), and
+    # two more for the breakdown (compute only, exchange only). gloo collectives run on the
+    # host and cannot be captured, so a gloo run (N > 1 ranks sharing one GPU) stays eager.
+    use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl")
+    graphs, per_step_launches = {}, 0
+    if use_graph:
+        for name, fn in (("step", step), ("compute", compute), ("exchange", exchange)):
+            if name == "exchange" and gather is None:
+                continue
+            g = torch.cuda.CUDAGraph()
+            launches[0] = 0
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            graphs[name] = g
+            if name == "step":
+                per_step_launches = launches[0]
+        torch.cuda.synchronize(dev)
+    run = {k: (lambda g=g: g.replay()) for k, g in graphs.items()} if use_graph else \
+        {"step": step, "compute": compute, "exchange": exchange}
+    if use_graph:
+        run["step"]()  # warm replay
+        torch.cuda.synchronize(dev)
     launches[0] = 0
+
+    def timed(fn, steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        for k in range(steps):
+            fn()
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        return [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+
     props = torch.cuda.get_device_properties(dev)
     gpu_id = f"GPU-{props.uuid}" if getattr(props, "uuid", None) else str(dev_index)
     clocks = ClockSampler(gpu_id)
     clocks.start()
     time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()  # timed region bracketed by barrier + synchronize on both sides
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for k in range(args.steps):
-        step(k)
-    t_end.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    step_ms = timed(run["step"], args.steps)  # the timed region: barrier + sync on both sides
     clk = clocks.stop()
-    total_ms = t_start.elapsed_time(t_end)
-    hist_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
-    step_ms = [ev[k][0].elapsed_time(ev[k][2]) for k in range(args.steps)]
-    t = torch.tensor([total_ms, float(np.mean(hist_ms))], dtype=torch.float64, device=dev)
-    rank_ms = [total_ms / args.steps]
+    gpu_launches = per_step_launches * args.steps if use_graph else launches[0]
+    total_ms = float(sum(step_ms))
+    # breakdown (after the timed region): the compute and the exchange alone, same K
+    comp_ms = timed(run["compute"], args.steps)
+    exch_ms = timed(run["exchange"], args.steps) if gather is not None else [0.0]
+    mine = [total_ms / args.steps, float(np.mean(comp_ms)), float(np.mean(exch_ms)), float(min(step_ms)),
+            float(statistics.median(step_ms))]
+    per_rank = [mine]
     if world > 1:
-        allr = torch.zeros(world, dtype=torch.float64, device=dev)
-        allr[rank] = total_ms / args.steps
-        dist.all_reduce(allr)  # per-rank ms/step (each rank fills its own slot)
-        rank_ms = allr.cpu().tolist()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max, hist_ms_max = float(t[0]), float(t[1])
-    gpu_launches = launches[0]
+        allr = torch.zeros((world, len(mine)), dtype=torch.float64, device=dev)
+        allr[rank] = torch.tensor(mine, dtype=torch.float64, device=dev)
+        dist.all_reduce(allr)  # each rank fills its own row
+        per_rank = allr.cpu().tolist()
+    ms_per_step = max(r[0] for r in per_rank)  # max over ranks
+    hist_ms_max = max(r[1] for r in per_rank)
 
     # ---- end-to-end through the public API from pinned host memory
     e2e = None
@@ -567,28 +638,32 @@ def run_b200(args):
         # runs the shot-diff (reads 2 rows, writes 4 B per position) when it is fused in
         diff_b = (e - jb) * (2 * 3 * bins * 4 + 4) if (do_diff and not do_ds) else 0
         alg_bytes = (e - jb + halo) * F + (e - jb) * (3 * bins * 4 + ds_b) + diff_b
-        achieved = alg_bytes / (hist_ms_max / 1e3) / 1e9
-        traffic, tsrc = traffic_from_profile(n, F, "histds" if do_ds else "hist")
-        ms_per_step = total_ms_max / args.steps
+        # the dominant call's average duration: at N = 1 the timed step IS that call (memset +
+        # histogram + shot-diff, replayed from the graph inside the timed region); at N > 1 the
+        # step also holds the exchange, so rank 0's compute-alone breakdown over the same K
+        launch_ms = per_rank[0][0] if world == 1 else per_rank[0][1]
+        achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+        traffic, tsrc = traffic_from_profile(n, F, "histds" if do_ds else "hist", scn.scn_version())
+        comp = [r[1] for r in per_rank]
         line = {
             "metric": METRIC, "value": M / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": wl.name, "frames": M, "frames_per_gpu": n, "width": wl.width, "height": wl.height, "bins": bins,
+            "config": {"workload": wl.name, "frames": M, "frames_per_gpu": n, "width": wl.width, "height": wl.height,
+                       "bins": bins,
                        "sampling": str(wl.sampling[:2] if wl.sampling[0] != "range" else ("range", len(wl.sampling[1]), wl.sampling[2])),
                        "ops": "+".join(ops) + (f"+adaptive_cuts(W={cut_w})" if cut_w else "") +
                               (("+fused_peer_gather" if p2p else "+nccl_allgather") if world > 1 else ""),
                        "content": args.mode, "parallelism": f"dp{world} contiguous shards + 1-frame halo",
-                       "hist_variant": ("tma_pair_lane_private" if bins in (1, 2, 4, 8, 16) else
-                                        "tma_single_shift_lane_private" if bins in (32, 64, 128, 256) else
-                                        "tma_single_lane_private"),
+                       "hist_variant": scn.scn_hist_variant(bins),
+                       "step_launch": "cuda_graph_replay" if use_graph else "eager",
                        "l2": "no flush: per-GPU input %.1f GB >> 126 MB L2" % (n * F / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("hist_tma_kernel<2,4,8,132> split layout (scn_run_hist_downsample incl. memset)" if do_ds else
-                                    "hist_tma_kernel<0,4,16,0> + shotdiff_kernel (scn_run_hist_shotdiff incl. "
-                                    "memset)" if do_diff else "hist_tma_kernel<0,4,16,0> (scn_run_histogram)"),
-                         "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": hist_ms_max,
+                         "kernel": ("hist_tma_kernel<2,8> fused hist+downsample (scn_run_hist_downsample incl. memset)"
+                                    if do_ds else "hist_tma_kernel<0,16> + shotdiff_kernel (scn_run_hist_shotdiff "
+                                    "incl. memset)" if do_diff else "hist_tma_kernel<0,16> (scn_run_histogram)"),
+                         "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": launch_ms,
                          "peak_source": peak_src, "traffic_source": tsrc,
                          # also against the nominal ~8 TB/s, and the second roofline
                          # (shared-atomic throughput of K2) next to its K0-measured capacity
@@ -600,10 +675,19 @@ def run_b200(args):
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clk,
-            "step_ms_min": float(min(step_ms)), "step_ms_median": float(statistics.median(step_ms)),
-            "rank_ms_per_step": rank_ms, "library": scn.scn_version(),
+            "step_ms_min": min(r[3] for r in per_rank), "step_ms_median": max(r[4] for r in per_rank),
+            # per-rank breakdown (ms per step): the step, its compute alone (memset + histogram +
+            # shot-diff), the exchange alone (all-gather), and the fixed cost step - compute
+            "breakdown": {"step_ms": [r[0] for r in per_rank], "compute_ms": comp,
+                          "gather_ms": [r[2] for r in per_rank],
+                          "overhead_ms": [r[0] - r[1] for r in per_rank],
+                          "barrier_skew_ms": max(comp) - min(comp)},
+            "library": scn.scn_version(),
         }
+        if gather_note:
+            line["config"]["gather_note"] = gather_note
         print(json.dumps(line), flush=True)
+    graphs.clear()
     job.close()
     if peer is not None:
         peer.close()
@@ -664,7 +748,7 @@ def run_e2e(args, wl, plan_, M, world, rank, dev, stream, ops, bins, do_diff, do
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    ksteps = max(1, min(args.steps, 5))
+    ksteps = max(1, min(args.steps, 10))
     e0.record(stream)
     for _ in range(ksteps):
         e2e_step()

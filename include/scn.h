@@ -193,7 +193,9 @@ scn_status scn_ipc_release(uint64_t d_base);
 /* 2x integer box downsample ("downsamples the resulting frames
  * (Resize)"): d_out[j] (u8, [end-begin][H/2][W/2][3]) with
  * O[y][x][c] = (P(2y,2x)+P(2y,2x+1)+P(2y+1,2x)+P(2y+1,2x+1)+2) >> 2; a
- * trailing odd row/column is dropped (reading Q11). */
+ * trailing odd row/column is dropped (reading Q11). Any width and any d_out
+ * alignment (byte granularity): W % 16 == 0 with an 8-byte aligned d_out takes
+ * the aligned row-pair kernel, everything else its realigning variant. */
 scn_status scn_run_downsample(const scn_seq* s, int64_t begin, int64_t end, uint8_t* d_out, void* stream);
 
 /* HIST + downsample of the same sampled frames in one read of each frame
@@ -208,8 +210,10 @@ scn_status scn_run_hist_downsample(const scn_seq* s, int64_t begin, int64_t end,
  * so the copy of chunk k+1 overlaps the kernels on chunk k (P:L248
  * "pipelining of CPU-GPU data transfers ... with graph operation execution").
  *   ops: bit 0 = HIST, bit 1 = shot-diff (needs HIST), bit 2 = downsample.
- *   d_staging: caller device memory, staging_bytes >= 2 * (ceil16(F) + 16)
- *              (two chunks of at least one frame each; more = larger chunks).
+ *   d_staging: caller device memory, 16-byte aligned, staging_bytes >=
+ *              ceil16(end - begin) + 2 * ceil16(F): the first ceil16(end-begin)
+ *              bytes hold the shard's segment-start flags, the rest two chunk
+ *              slots of at least one frame each (more = larger chunks).
  *   d_scratch: >= 3*bins u32 when shot-diff needs a halo.
  *   copy_stream: second stream for the H2D copies (may equal stream).
  * Outputs as the device-location calls. Only enqueues work (host frames
@@ -258,7 +262,9 @@ scn_status scn_run_diff_pairs(const uint32_t* d_hist, const int64_t* d_a, const 
  * scn_run_adaptive_cuts: d_diff holds D for positions [wb, end) (e.g. from
  * scn_run_hist_shotdiff over [wb, end), whose own [-1,0] halo is recomputed);
  * d_cut (u8, [end-begin]) gets the flags for [begin, end) only — the warmup
- * outputs are never written. EINVAL if warmup < 1 or k_den < 1.
+ * outputs are never written. EINVAL if warmup < 1, k_den < 1 or
+ * warmup * (k_num + k_den) >= 2^32 (the bound that keeps both sides of the
+ * comparison below 2^64, so it is exact).
  * ------------------------------------------------------------------------- */
 int64_t scn_seq_warmup_begin(const scn_seq* s, int64_t begin, int32_t warmup);
 scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, int32_t warmup,
@@ -291,9 +297,28 @@ scn_status scn_run_montage(const scn_seq* s, int64_t begin, int64_t end, int32_t
                            int64_t canvas_pitch, void* stream);
 
 /* Launch statistics for the last scn_run_* call on this thread: number of
- * kernels launched and the histogram kernel variant used (for bench.py's
- * gpu_launches count). */
+ * kernels launched (for bench.py's gpu_launches count). */
 int32_t scn_last_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Histogram implementation for bins dividing 16 (process-wide; results are
+ * identical, only the speed differs — DESIGN.md §5):
+ *   SCN_HIST_LANE_PAIRS   (default) lane-private pair-key bins, 0.5 shared
+ *                         atomics per byte, one global merge per CTA and frame;
+ *   SCN_HIST_MATCH        north_star's per-warp bins with __match_any_sync
+ *                         aggregation per byte (K2a);
+ *   SCN_HIST_MATCH_PACKED K2a with one __match_any_sync per packed word of four
+ *                         pair keys (K2a').
+ * Other bin counts always take the raw-value kernel (any B in [1,256], bins
+ * merged at the per-frame flush). EINVAL for an unknown value.
+ * scn_hist_variant names the kernel a run with `bins` takes.
+ * ------------------------------------------------------------------------- */
+#define SCN_HIST_LANE_PAIRS 0
+#define SCN_HIST_MATCH 1
+#define SCN_HIST_MATCH_PACKED 2
+scn_status scn_set_hist_impl(int32_t impl);
+int32_t scn_get_hist_impl(void);
+const char* scn_hist_variant(int32_t bins);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscn.so")
+# SCN_LIB=tuning loads the measurement build (same kernels + SCN_* environment knobs, `make tuning`)
+LIB_PATH = os.path.join(_HERE, "libscn_tuning.so" if os.environ.get("SCN_LIB") == "tuning" else "libscn.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {os.path.dirname(_HERE)}` "
                       "(no CPU fallback exists)")
@@ -23,6 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 SCN_OK, SCN_EINVAL, SCN_ERANGE, SCN_ECUDA, SCN_EUNSUPPORTED = 0, 1, 2, 3, 4
 SCN_MEM_DEVICE, SCN_MEM_HOST = 0, 1
 SCN_OP_HIST, SCN_OP_SHOTDIFF, SCN_OP_DOWNSAMPLE = 1, 2, 4
+SCN_HIST_LANE_PAIRS, SCN_HIST_MATCH, SCN_HIST_MATCH_PACKED = 0, 1, 2
 STATUS_NAMES = {0: "SCN_OK", 1: "SCN_EINVAL", 2: "SCN_ERANGE", 3: "SCN_ECUDA", 4: "SCN_EUNSUPPORTED"}
 
 _vp = ctypes.c_void_p
@@ -47,6 +49,9 @@ _pp = ctypes.POINTER(_vp)
 _sig("scn_last_error", ctypes.c_char_p)
 _sig("scn_version", ctypes.c_char_p)
 _sig("scn_last_launch_count", _i32)
+_sig("scn_set_hist_impl", ctypes.c_int, _i32)
+_sig("scn_get_hist_impl", _i32)
+_sig("scn_hist_variant", ctypes.c_char_p, _i32)
 _sig("scn_table_create", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _i64, _vp, _pp)
 _sig("scn_table_destroy", None, _vp)
 _sig("scn_table_rows", _i64, _vp)
@@ -120,6 +125,18 @@ def scn_version() -> str:
 
 def scn_last_launch_count() -> int:
     return int(_lib.scn_last_launch_count())
+
+
+def scn_set_hist_impl(impl: int) -> None:
+    _check(_lib.scn_set_hist_impl(impl), "scn_set_hist_impl")
+
+
+def scn_get_hist_impl() -> int:
+    return int(_lib.scn_get_hist_impl())
+
+
+def scn_hist_variant(bins: int) -> str:
+    return _lib.scn_hist_variant(bins).decode()
 
 
 def scn_table_create(num_rows, width, height, channels=3, where=SCN_MEM_DEVICE, base=None, frame_stride_bytes=0,
@@ -269,6 +286,8 @@ def scn_run_adaptive_cuts(s, begin, end, warmup, d_diff, k_num, k_den, floor, d_
 def scn_select_shot_starts(s, begin, end, h_diff, tau) -> np.ndarray:
     """NEXT N1: positions in [begin,end) that start a shot (segment start or D > tau)."""
     d = np.ascontiguousarray(h_diff, dtype=np.uint32)
+    if end > begin and len(d) < end - begin:
+        raise ValueError(f"h_diff holds {len(d)} values, the range [{begin},{end}) needs {end - begin}")
     cnt = _i64()
     _check(_lib.scn_select_shot_starts(s, begin, end, d.ctypes.data, tau, None, 0, ctypes.byref(cnt)),
            "scn_select_shot_starts")
@@ -296,6 +315,8 @@ def scn_run_hist_shotdiff_to(s, begin, end, bins, hist_dests, diff_dests, self_i
     """HIST + shot-diff writing rows [begin,end) straight into every rank's result columns."""
     h = np.ascontiguousarray(hist_dests, dtype=np.uint64)
     d = np.ascontiguousarray(diff_dests, dtype=np.uint64)
+    if len(h) != len(d):
+        raise ValueError(f"{len(h)} histogram destinations but {len(d)} diff destinations")
     _check(_lib.scn_run_hist_shotdiff_to(s, begin, end, bins, h.ctypes.data, d.ctypes.data, len(h), self_index,
                                          _ptr(d_scratch), _stream(stream)), "scn_run_hist_shotdiff_to")
 

@@ -33,19 +33,17 @@ struct DestList {
 };
 // zero `words` u32 at each destination (peer stores for mapped peers)
 cudaError_t launch_zero_dests(const DestList& d, int64_t words, cudaStream_t st, int* launches);
-// shot-diff over n positions writing D[p] to every d.p[g] + p (u32)
-cudaError_t launch_shotdiff_dests(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
-                                  int32_t bins, const DestList& d, cudaStream_t st, int* launches);
 
 // Histogram (zeroes nothing: the caller memsets out/halo_out first).
 // Returns the number of kernel launches in *launches.
 cudaError_t launch_histogram(const HistJob& job, cudaStream_t st, int* launches);
 // Fused HIST + downsample; falls back to two passes for shapes the fused kernel does not take.
 cudaError_t launch_hist_downsample(const HistJob& job, cudaStream_t st, int* launches);
-// Shot-diff over n positions; seg[p] != 0 marks a segment start; halo_row is the
-// histogram of the position before the first (used iff !seg[0]).
+// Shot-diff over n positions, D[p] written to every d.p[g] + p (d.n = 1 for a plain run);
+// seg[p] != 0 marks a segment start; halo_row is the histogram of the position before the
+// first (used iff !seg[0]).
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
-                            int32_t bins, uint32_t* diff, cudaStream_t st, int* launches);
+                            int32_t bins, const DestList& d, cudaStream_t st, int* launches);
 // D[j] = sum |H[a[j]] - H[b[j]]| (NEXT N2: stencil before sampling)
 cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int64_t* b, int64_t n, int32_t bins,
                               uint32_t* diff, cudaStream_t st, int* launches);
@@ -55,8 +53,13 @@ cudaError_t launch_adaptive_cuts(const uint32_t* diff, const uint8_t* seg, int64
                                  uint32_t k_num, uint32_t k_den, uint32_t floor_, uint8_t* cut, cudaStream_t st,
                                  int* launches);
 cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int32_t height, uint8_t* out,
-                              cudaStream_t st, int* launches, int64_t ds_pitch = 0, int32_t ds_cols = 0,
-                              bool allow_vec = true);
+                              cudaStream_t st, int* launches, int64_t ds_pitch = 0, int32_t ds_cols = 0);
+
+// Histogram implementation (scn_set_hist_impl): 0 = lane-private pair keys (default),
+// 1 = the north_star's per-warp bins + __match_any_sync per byte (K2a), 2 = K2a with one
+// MATCH per packed word of four pair keys (K2a'). Applies to bins dividing 16.
+void set_hist_impl(int impl);
+int hist_impl();
 
 // Variant names for reporting
 const char* hist_variant_name(int32_t bins);

@@ -71,6 +71,14 @@ const char* scn_last_error(void) { return g_err.c_str(); }
 const char* scn_version(void) { return "scn-b200 0.1 (sm_100a, " SCN_GIT_SHA ")"; }
 int32_t scn_last_launch_count(void) { return g_launches; }
 
+scn_status scn_set_hist_impl(int32_t impl) {
+  if (impl < SCN_HIST_LANE_PAIRS || impl > SCN_HIST_MATCH_PACKED) return fail(SCN_EINVAL, "unknown hist impl %d", impl);
+  scn::set_hist_impl(impl);
+  return SCN_OK;
+}
+int32_t scn_get_hist_impl(void) { return scn::hist_impl(); }
+const char* scn_hist_variant(int32_t bins) { return scn::hist_variant_name(bins); }
+
 // ---------------------------------------------------------------------------
 // tables
 // ---------------------------------------------------------------------------
@@ -369,6 +377,9 @@ scn_status scn_run_adaptive_cuts(const scn_seq* s, int64_t begin, int64_t end, i
   scn_status rc = check_run(s, begin, end, 1, false);
   if (rc) return rc;
   if (warmup < 1 || k_den < 1) return fail(SCN_EINVAL, "warmup and k_den must be >= 1");
+  // both sides of the test are < 2^64 iff W * (k_num + k_den) < 2^32 (D, floor < 2^32)
+  if ((uint64_t)warmup * ((uint64_t)k_num + k_den) >= (1ull << 32))
+    return fail(SCN_EINVAL, "warmup * (k_num + k_den) must be < 2^32 (64-bit exact comparison)");
   if (end == begin) return SCN_OK;
   if (!d_diff || !d_cut) return fail(SCN_EINVAL, "d_diff/d_cut is NULL");
   const int64_t wb = scn_seq_warmup_begin(s, begin, warmup);
@@ -459,6 +470,13 @@ static scn_status check_resident(const scn_seq* s, int64_t first, int64_t end) {
   return SCN_OK;
 }
 
+static scn::DestList one_dest(uint32_t* p) {
+  scn::DestList d{};
+  d.n = 1;
+  d.p[0] = (uint64_t)(uintptr_t)p;
+  return d;
+}
+
 static const uint64_t* d_addr(const scn_seq* s) { return (const uint64_t*)s->d_ws; }
 static const uint8_t* d_seg(const scn_seq* s) { return (const uint8_t*)s->d_ws + 8 * s->addr.size(); }
 
@@ -499,7 +517,7 @@ scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32
 static scn_status run_diff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, const uint32_t* d_hist,
                            const uint32_t* halo, uint32_t* d_diff, cudaStream_t st) {
   int nl = 0;
-  cudaError_t e = scn::launch_shotdiff(d_hist, halo, d_seg(s) + begin, end - begin, bins, d_diff, st, &nl);
+  cudaError_t e = scn::launch_shotdiff(d_hist, halo, d_seg(s) + begin, end - begin, bins, one_dest(d_diff), st, &nl);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "shotdiff launch");
   return SCN_OK;
@@ -583,8 +601,8 @@ scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end
   for (int32_t g = 0; g < n_dest; ++g) j.dest[g] = dh.p[g];
   e = scn::launch_histogram(j, st, &nl);
   if (e == cudaSuccess)
-    e = scn::launch_shotdiff_dests(reinterpret_cast<const uint32_t*>(dh.p[self]), halo ? d_scratch : nullptr,
-                                   d_seg(s) + begin, n, bins, dd, st, &nl);
+    e = scn::launch_shotdiff(reinterpret_cast<const uint32_t*>(dh.p[self]), halo ? d_scratch : nullptr,
+                             d_seg(s) + begin, n, bins, dd, st, &nl);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "hist_shotdiff_to launch");
   return SCN_OK;
@@ -638,11 +656,10 @@ scn_status scn_run_montage(const scn_seq* s, int64_t begin, int64_t end, int32_t
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(d_canvas, 0, (size_t)(tile_rows * oh * canvas_pitch), st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(canvas)");
-  // 8-byte vector stores need 8-aligned tiles; other layouts take the bytewise kernel
-  const bool aligned = ((uintptr_t)d_canvas % 8 == 0) && canvas_pitch % 8 == 0 && ow3 % 8 == 0;
+  // any canvas alignment: unaligned tiles take the kernel's realigned-store path
   scn::FrameSrc src{d_addr(s) + begin, 0, 0};
   int nl = 0;
-  e = scn::launch_downsample(src, k, s->width, s->height, d_canvas, st, &nl, canvas_pitch, cols, aligned);
+  e = scn::launch_downsample(src, k, s->width, s->height, d_canvas, st, &nl, canvas_pitch, cols);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "montage launch");
   return SCN_OK;
@@ -770,7 +787,8 @@ scn_status scn_run_pipeline_host(const scn_seq* s, int64_t begin, int64_t end, i
   }
   if (e == cudaSuccess && do_diff) {
     int nl = 0;
-    e = scn::launch_shotdiff(d_hist, halo ? d_scratch : nullptr, (const uint8_t*)d_staging, n, bins, d_diff, st, &nl);
+    e = scn::launch_shotdiff(d_hist, halo ? d_scratch : nullptr, (const uint8_t*)d_staging, n, bins,
+                             one_dest(d_diff), st, &nl);
     g_launches += nl;
   }
   for (int i = 0; i < 2; ++i) {

@@ -231,37 +231,42 @@ class HostJob:
 
 
 class ColumnGather:
-    """Final result exchange for N > 1: each rank's shard rows of
-    H [n,3,B] and D [n] are packed into one padded [ceil(M/G), 3B+1] int32 block and
-    all-gathered in ONE collective (NCCL on the GPU box, gloo in the CPU tests);
-    result() unpacks and trims the padding."""
+    """Final result exchange for N > 1: ONE all-gather of a flat int32
+    send block laid out [rows_pad x 3B histogram counters | rows_pad shot-diffs], rows_pad =
+    ceil(M/G). The kernels write the shard's H and D straight into the block through the
+    `hist` / `diff` views (no pack copies); gather() copies only when handed other buffers.
+    NCCL on the GPU box, gloo in the CPU tests; result() unpacks and trims the padding."""
 
     def __init__(self, M: int, world: int, bins: int, device, dist):
         self.M, self.world, self.bins, self.dist = M, world, bins, dist
-        self.rows_pad = -(-M // world) if world else 0
+        self.rows_pad = max(-(-M // world), 1) if world else 1
         self.spans = [scn.scn_shard_range(M, world, r) for r in range(world)]
-        self.K = 3 * bins + 1
-        self.pad = torch.zeros((self.rows_pad, self.K), dtype=torch.int32, device=device)
-        self.all = torch.empty((self.rows_pad * world, self.K), dtype=torch.int32, device=device)
+        self.K = 3 * bins
+        self.block = self.rows_pad * (self.K + 1)
+        self.send = torch.zeros(self.block, dtype=torch.int32, device=device)
+        self.hist = self.send[: self.rows_pad * self.K].view(self.rows_pad, 3, bins)
+        self.diff = self.send[self.rows_pad * self.K:]
+        self.all = torch.empty(self.block * world, dtype=torch.int32, device=device)
 
-    def gather(self, hist, diff, n: int):
-        self.pad[:n, : 3 * self.bins].copy_(hist[:n].reshape(n, 3 * self.bins))
-        if diff is not None:
-            self.pad[:n, 3 * self.bins].copy_(diff[:n])
-        if self.pad.is_cuda and self.dist.get_backend() == "gloo":
+    def gather(self, hist=None, diff=None, n: int = 0):
+        if hist is not None and hist.data_ptr() != self.hist.data_ptr():
+            self.hist[:n].copy_(hist[:n].reshape(n, 3, self.bins))
+        if diff is not None and diff.data_ptr() != self.diff.data_ptr():
+            self.diff[:n].copy_(diff[:n])
+        if self.send.is_cuda and self.dist.get_backend() == "gloo":
             # test-only path (several ranks sharing one GPU): gloo gathers host copies
-            pa, aa = self.pad.cpu(), self.all.cpu()
+            pa, aa = self.send.cpu(), self.all.cpu()
             self.dist.all_gather_into_tensor(aa, pa)
             self.all.copy_(aa)
             return
-        self.dist.all_gather_into_tensor(self.all, self.pad)
+        self.dist.all_gather_into_tensor(self.all, self.send)
 
     def result(self):
+        a = self.all.view(self.world, self.block)
         hs, ds = [], []
         for r, (b, e) in enumerate(self.spans):
-            o = r * self.rows_pad
-            hs.append(self.all[o:o + e - b, : 3 * self.bins].reshape(e - b, 3, self.bins))
-            ds.append(self.all[o:o + e - b, 3 * self.bins])
+            hs.append(a[r, : (e - b) * self.K].reshape(e - b, 3, self.bins))
+            ds.append(a[r, self.rows_pad * self.K: self.rows_pad * self.K + e - b])
         return torch.cat(hs), torch.cat(ds)
 
 

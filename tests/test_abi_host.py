@@ -340,3 +340,49 @@ def test_pipeline_host_validation_without_gpu():
     assert e.value.status == scn.SCN_ERANGE
     scn.scn_seq_destroy(q)
     scn.scn_table_destroy(t)
+
+
+def test_adaptive_cuts_overflow_bound_and_hist_impl_validation():
+    # W * (k_num + k_den) must stay < 2^32 so the 64-bit comparison is exact (DESIGN §8 N3)
+    t = _table(10)
+    q = scn.scn_sample_stride(t, 1)
+    scn.scn_run_adaptive_cuts(q, 0, 0, 16, None, 4, 1, 0, None)  # in bounds, empty range: no-op
+    for w, kn, kd in ((1 << 16, 1 << 16, 0), (2, (1 << 31), (1 << 31) - 1), (1 << 30, 2, 2)):
+        with pytest.raises(scn.ScnError) as e:
+            scn.scn_run_adaptive_cuts(q, 0, 0, w, None, kn, max(kd, 1), 0, None)
+        assert e.value.status == scn.SCN_EINVAL
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)
+    assert scn.scn_get_hist_impl() == scn.SCN_HIST_LANE_PAIRS
+    for bad in (-1, 3):
+        with pytest.raises(scn.ScnError) as e:
+            scn.scn_set_hist_impl(bad)
+        assert e.value.status == scn.SCN_EINVAL
+    assert scn.scn_hist_variant(16) == "tma_pair_lane_private"
+    assert scn.scn_hist_variant(100) == "tma_raw_lane_private_remap"
+    scn.scn_set_hist_impl(scn.SCN_HIST_MATCH_PACKED)
+    assert scn.scn_hist_variant(8) == "k2a_packed_match_per_warp"
+    assert scn.scn_hist_variant(256) == "tma_raw_lane_private_remap"
+    scn.scn_set_hist_impl(scn.SCN_HIST_LANE_PAIRS)
+
+
+def test_binding_rejects_short_host_arrays():
+    t = _table(10)
+    q = scn.scn_sample_stride(t, 1)
+    with pytest.raises(ValueError):
+        scn.scn_select_shot_starts(q, 0, 5, np.zeros(4, np.uint32), 1)
+    with pytest.raises(ValueError):
+        scn.scn_run_hist_shotdiff_to(q, 0, 0, 16, [1 << 20, 1 << 21], [1 << 22], 0)
+    scn.scn_seq_destroy(q)
+    scn.scn_table_destroy(t)
+
+
+def test_product_library_reads_no_environment():
+    # the measurement knobs exist only in libscn_tuning.so (-DSCN_TUNING); outside that
+    # #ifdef block the product sources call no getenv (cudart_static's own are not ours)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_1805_07339_b200", "csrc", "kernels.cu")).read()
+    pre, rest = src.split("#ifdef SCN_TUNING", 1)
+    tuning, post = rest.split("#else", 1)
+    assert "getenv" in tuning and "getenv" not in pre + post
+    assert "getenv" not in open(os.path.join(root, "paper_1805_07339_b200", "csrc", "scn_api.cpp")).read()

@@ -4,6 +4,7 @@ import pytest
 import torch
 
 import oracle
+import paper_1805_07339_b200 as scn
 import scn_harness
 import scn_synth
 from scn_synth import Workload
@@ -27,10 +28,19 @@ def test_n2_stencil_then_sample(sampling, offset):
     got = _u32(out["diff"])[: job.M]
     expect = oracle.stencil_then_sample(wl.spec(), job.part, job.row, offset, wl.rows_per_video, wl.bins)
     np.testing.assert_array_equal(got, expect)
-    # the required set is exactly the oracle's dependency closure, per table
+    # the materialised required set is exactly the oracle's dependency closure, per table
+    # (scn_seq_stencil_required numbers the tables that hold sampled rows 0, 1, ... in order)
+    req_part, req_row = scn.scn_seq_rows(job.req)
+    total, k = 0, 0
     for v in range(wl.n_videos):
         rows = job.row[job.part == v]
-        assert len(oracle.required_rows(rows, offset, wl.rows_per_video)) > 0
+        if len(rows) == 0:
+            continue
+        expect = oracle.required_rows(rows, offset, wl.rows_per_video)
+        np.testing.assert_array_equal(req_row[req_part == k], expect)
+        total += len(expect)
+        k += 1
+    assert job.R == total == len(req_row)
     job.close()
 
 

@@ -1,6 +1,12 @@
-"""Tuning sweep for the histogram kernel (not part of the product): times
-scn_run_histogram on C2-shaped frames for one knob setting (env SCN_HIST_WARPS /
-SCN_HIST_TILE are read by libscn.so) and content mode; prints one JSON line."""
+"""Kernel timing for measurement runs (not part of the product): times one library call
+(hist | histds | ds) over `frames` sampled frames of a config, optionally at another frame
+size, bin count or histogram impl, and prints one JSON line with the median rate in
+algorithmic GB/s. The measurement build's SCN_* knobs apply with SCN_LIB=tuning.
+
+    python tools/hist_tune.py MODE FRAMES CFG OP [--bins B] [--shape WxH] [--impl I] [--reps R] [--offset O]
+"""
+import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -15,41 +21,59 @@ import scn_synth  # noqa: E402
 
 
 def main():
-    mode = sys.argv[1] if len(sys.argv) > 1 else "shots"
-    frames = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
-    cfg = sys.argv[3] if len(sys.argv) > 3 else "C2"
-    op = sys.argv[4] if len(sys.argv) > 4 else "hist"
-    wl = scn_synth.WORKLOADS[cfg]
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", nargs="?", default="shots")
+    ap.add_argument("frames", nargs="?", type=int, default=4096)
+    ap.add_argument("cfg", nargs="?", default="C2")
+    ap.add_argument("op", nargs="?", default="hist", choices=["hist", "histds", "ds"])
+    ap.add_argument("--bins", type=int, default=0)
+    ap.add_argument("--shape", default="")
+    ap.add_argument("--impl", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=int(os.environ.get("REPS", "7")))
+    ap.add_argument("--offset", type=int, default=0, help="byte offset of the downsample output (alignment)")
+    a = ap.parse_args()
+    wl = scn_synth.WORKLOADS[a.cfg]
+    if a.bins:
+        wl = dataclasses.replace(wl, bins=a.bins)
+    if a.shape:
+        w, h = (int(x) for x in a.shape.lower().split("x"))
+        wl = dataclasses.replace(wl, width=w, height=h)
+    scn.scn_set_hist_impl(a.impl)
     pl = scn_harness.plan(wl)
-    frames = min(frames, len(pl[1]))
-    job = scn_harness.DeviceJob(wl, 0, frames, with_halo=False, spec=wl.spec(mode=mode), plan_=pl)
-    out = job.alloc_outputs(("hist", "downsample"), wl.bins)
+    frames = min(a.frames, len(pl[1]))
+    job = scn_harness.DeviceJob(wl, 0, frames, with_halo=False, spec=wl.spec(mode=a.mode), plan_=pl)
+    out = job.alloc_outputs(("hist",), wl.bins)
+    dsb = frames * (wl.height // 2) * (wl.width // 2) * 3
+    ds = torch.empty(dsb + 16, dtype=torch.uint8, device="cuda") if a.op != "hist" else None
+    dptr = ds.data_ptr() + a.offset if ds is not None else None
     st = torch.cuda.current_stream()
 
     def call():
-        if op == "hist":
+        if a.op == "hist":
             scn.scn_run_histogram(job.seq, 0, frames, wl.bins, out["hist"], st)
-        elif op == "histds":
-            scn.scn_run_hist_downsample(job.seq, 0, frames, wl.bins, out["hist"], out["ds"], st)
+        elif a.op == "histds":
+            scn.scn_run_hist_downsample(job.seq, 0, frames, wl.bins, out["hist"], dptr, st)
         else:
-            scn.scn_run_downsample(job.seq, 0, frames, out["ds"], st)
+            scn.scn_run_downsample(job.seq, 0, frames, dptr, st)
 
     for _ in range(3):
         call()
     ts = []
-    for _ in range(int(os.environ.get("REPS", "7"))):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
         call()
-        b.record(st)
+        e1.record(st)
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
+        ts.append(e0.elapsed_time(e1))
     ms = sorted(ts)[len(ts) // 2]
-    per = wl.frame_bytes * (1.0 if op == "hist" else 1.25)  # algorithmic bytes: read F (+ write F/4)
-    gbs = frames * per / (ms / 1e3) / 1e9
-    print(json.dumps({"cfg": cfg, "op": op, "fused_tile": os.environ.get("SCN_FUSED_TILE", ""), "mode": mode, "frames": frames, "warps": os.environ.get("SCN_HIST_WARPS", "16"),
-                      "tile": os.environ.get("SCN_HIST_TILE", "30720"), "ms": ms, "GBps": gbs,
-                      "min_ms": min(ts), "all": [round(x, 3) for x in ts]}), flush=True)
+    F = wl.frame_bytes
+    alg = frames * F + (dsb if a.op != "hist" else 0) + (frames * 3 * wl.bins * 4 if a.op != "ds" else 0)
+    print(json.dumps({"cfg": a.cfg, "op": a.op, "mode": a.mode, "frames": frames, "width": wl.width,
+                      "height": wl.height, "bins": wl.bins, "impl": a.impl, "offset": a.offset,
+                      "variant": scn.scn_hist_variant(wl.bins), "ms": ms, "GBps": alg / (ms / 1e3) / 1e9,
+                      "min_ms": min(ts), "all": [round(x, 3) for x in ts], "library": scn.scn_version(),
+                      "knobs": {k: v for k, v in os.environ.items() if k.startswith("SCN_")}}), flush=True)
     job.close()
 
 

@@ -3,7 +3,7 @@ into the derived quantities SURVEY §8(d) asks for: DRAM bytes vs algorithmic by
 instructions and shared atomics per input byte, atomic bank conflicts, lane-atomics per
 SM-clock, issue utilisation and the stall breakdown. Prints one JSON object.
 
-    python tools/ncu_summarize.py counters.csv NAME FRAMES CFG OP
+    python tools/ncu_summarize.py counters.csv NAME FRAMES CFG OP [BINS] [WxH] [GIT_SHA]
 """
 import csv
 import json
@@ -36,15 +36,24 @@ def main():
     frames = int(frames)
     v, kernel = read(path)
     wl = scn_synth.WORKLOADS[cfg]
+    import dataclasses
+    if len(sys.argv) > 6 and int(sys.argv[6]):
+        wl = dataclasses.replace(wl, bins=int(sys.argv[6]))
+    if len(sys.argv) > 7 and sys.argv[7]:
+        w, h = (int(x) for x in sys.argv[7].lower().split("x"))
+        wl = dataclasses.replace(wl, width=w, height=h)
+    sha = sys.argv[8] if len(sys.argv) > 8 else None
     F = wl.frame_bytes
     in_bytes = frames * F
-    alg = in_bytes + (frames * F // 4 if op != "hist" else 0) + (frames * 3 * wl.bins * 4 if op != "ds" else 0)
+    dsb = frames * (wl.height // 2) * (wl.width // 2) * 3
+    alg = in_bytes + (dsb if op != "hist" else 0) + (frames * 3 * wl.bins * 4 if op != "ds" else 0)
     t = v["gpu__time_duration.sum"] * 1e-9 if v.get("gpu__time_duration.sum") else None  # ns
     rd, wr = v.get("dram__bytes_read.sum", 0.0), v.get("dram__bytes_write.sum", 0.0)
     cyc = v.get("sm__cycles_elapsed.avg")
     atom = v.get("smsp__inst_executed_op_shared_atom.sum", 0.0)
     out = {
         "kernel": kernel, "capture": os.path.basename(path), "config": cfg, "op": op, "frames": frames,
+        "bins": wl.bins, "width": wl.width, "height": wl.height, "git_sha": sha,
         "frame_bytes": F, "algorithmic_bytes": alg,
         "dram_read_bytes": rd, "dram_write_bytes": wr,
         "dram_over_algorithmic": (rd + wr) / alg,
