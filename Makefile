@@ -23,7 +23,7 @@ MICRO      := tools/micro/k0
 DEMO       := examples/scn_demo
 CUDA_HOME  ?= /usr/local/cuda
 
-all: $(LIB) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(DEMO)
+all: $(LIB) $(LIB_TUNE) $(SYNTH_HOST) $(SYNTH_CUDA) $(ORACLE) $(DEMO)
 
 lib: $(LIB)
 # measurement build: the same kernels with the SCN_* environment knobs (grid, tiles,

@@ -18,6 +18,9 @@ import scn_synth  # noqa: E402
 from scn_synth import Workload  # noqa: E402
 
 
+VERBOSE = os.environ.get("SCN_TEST_VERBOSE") == "1"
+
+
 def main():
     impl = int(os.environ.get("SCN_TEST_HIST_IMPL", "0"))
     scn.scn_set_hist_impl(impl)
@@ -37,6 +40,8 @@ def main():
             job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, spec=spec, plan_=pl)
             out = job.alloc_outputs(("hist", "shotdiff", "downsample"), wl.bins)
             for ops, fused in ((("hist", "shotdiff"), True), (("hist", "downsample"), True), (("downsample",), False)):
+                if VERBOSE:
+                    print("case", wl.name, mode, ops, flush=True)
                 job.run(out, ops, wl.bins, fused=fused)
                 torch.cuda.synchronize()
                 if "hist" in ops:
@@ -55,6 +60,8 @@ def main():
                 H, D, _ = oracle.run(spec, pl[0], pl[1], pl[2], 0, M, bins)
                 job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, spec=spec, plan_=pl)
                 out = job.alloc_outputs(("hist", "shotdiff"), bins)
+                if VERBOSE:
+                    print("case", wl.name, mode, bins, flush=True)
                 job.run(out, ("hist", "shotdiff"), bins)
                 torch.cuda.synchronize()
                 assert (out["hist"].cpu().numpy().view(np.uint32)[:M] == H).all(), (wl.name, mode, bins)
