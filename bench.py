@@ -546,19 +546,31 @@ def run_b200(args):
     # two more for the breakdown (compute only, exchange only). gloo collectives run on the
     # host and cannot be captured, so a gloo run (N > 1 ranks sharing one GPU) stays eager.
     use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl")
-    graphs, per_step_launches = {}, 0
+    graphs, per_step_launches, graph_note = {}, 0, None
     if use_graph:
-        for name, fn in (("step", step), ("compute", compute), ("exchange", exchange)):
-            if name == "exchange" and gather is None:
-                continue
-            g = torch.cuda.CUDAGraph()
-            launches[0] = 0
-            with torch.cuda.graph(g, stream=stream):
-                fn()
-            graphs[name] = g
-            if name == "step":
-                per_step_launches = launches[0]
-        torch.cuda.synchronize(dev)
+        try:
+            for name, fn in (("step", step), ("compute", compute), ("exchange", exchange)):
+                if name == "exchange" and gather is None:
+                    continue
+                g = torch.cuda.CUDAGraph()
+                launches[0] = 0
+                with torch.cuda.graph(g, stream=stream):
+                    fn()
+                graphs[name] = g
+                if name == "step":
+                    per_step_launches = launches[0]
+            torch.cuda.synchronize(dev)
+        except Exception as ex:  # noqa: BLE001 (reported; the step then launches eagerly)
+            graph_note = f"graph capture failed, eager launches: {type(ex).__name__}: {ex}"[:200]
+            graphs.clear()
+            torch.cuda.synchronize(dev)
+        if world > 1:  # every rank takes the same path
+            ok = torch.tensor([0.0 if graphs else 1.0], dtype=torch.float64, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+            if float(ok[0]):
+                graphs.clear()
+                graph_note = graph_note or "graph capture failed on another rank, eager launches"
+        use_graph = bool(graphs)
     run = {k: (lambda g=g: g.replay()) for k, g in graphs.items()} if use_graph else \
         {"step": step, "compute": compute, "exchange": exchange}
     if use_graph:
@@ -686,6 +698,8 @@ def run_b200(args):
         }
         if gather_note:
             line["config"]["gather_note"] = gather_note
+        if graph_note:
+            line["config"]["graph_note"] = graph_note
         print(json.dumps(line), flush=True)
     graphs.clear()
     job.close()

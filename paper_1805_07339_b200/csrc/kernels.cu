@@ -60,6 +60,11 @@ constexpr int kVarGen = 1;  // row-pair modes: any width / output alignment
 
 constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 producer warp)
 constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only kernels
+// kVarGen kernels: more warps hide the longer dependency chains of the realigned loads and
+// stores (measured, profiles/r02_tune_gen.jsonl: ds-only 1366x768 5.51 / 6.32 / 6.76 TB/s with
+// 8 / 12 / 16 warps; fused 4.12 / 4.96 / 4.92)
+constexpr int kGenDsWarps = 16;
+constexpr int kGenFusedWarps = 12;
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
                                    // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
 constexpr uint32_t kGenSlack = 64;  // kVarGen slots: 15 B of leading misalignment + 15 B rounding + 16 B overread
@@ -91,6 +96,7 @@ struct HistParams {
   uint32_t table_align;
   int32_t l2_prefetch;  // > 0: the producer bulk-prefetches tile t + l2_prefetch into L2
   int32_t max_stages;   // cap on the ring depth
+  uint32_t prod_sleep;  // > 0: the producer waits for a free slot with this suspend-time hint (ns)
   int32_t n_dest;       // > 0: results go to every dest[g] (fused all-gather over peer memory)
   uint64_t dest[kMaxDest];
 };
@@ -318,36 +324,48 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) { 
   d[1] = make_uint2(o[2], o[3]);
   d[2] = make_uint2(o[4], o[5]);
 }
-__device__ __forceinline__ void st_bytes(uint8_t* dst, uint64_t x, uint32_t n) {  // the low n bytes of x
-  for (uint32_t i = 0; i < n; ++i) dst[i] = (uint8_t)(x >> (8 * i));
-}
 // 24 output bytes at ANY address (kVarGen). Lanes of one row write consecutive 24-byte
-// chunks; each lane stores the aligned 8-byte words that START inside its chunk — the
-// third one ends in the next lane's chunk, whose first 8 bytes come by one shuffle pair.
-// Bytes of a word whose neighbour is missing (row ends, warp edges, idle lanes) are stored
-// bytewise. All 32 lanes call this (full-warp shuffles); only `act` lanes store.
+// chunks; each lane stores the three aligned 8-byte words that START inside its chunk —
+// when the chunk is not 8-aligned the third one ends in the next lane's chunk, whose first
+// 8 bytes come by one shuffle pair. The words are cut from the 32-bit stream (o, next) by
+// funnel shifts after a select on the word offset, so every lane runs the same code for
+// any alignment. Bytes of a word whose neighbour is missing (row ends, warp edges, idle
+// lanes) are written as naturally aligned 1/2/4-byte pieces. All 32 lanes call this
+// (full-warp shuffles); only `act` lanes store.
 __device__ __forceinline__ void st_global_24_any(uint8_t* dst, const uint32_t* o, bool act, bool has_next,
                                                  bool has_prev) {
   const uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, o[0], 1), n1 = __shfl_down_sync(0xFFFFFFFFu, o[1], 1);
   if (!act) return;
-  const uint32_t a = (uint32_t)(uintptr_t)dst & 7u;
-  if (a == 0) {
-    st_global_24(dst, o);
-    return;
+  const uint32_t b = (8u - ((uint32_t)(uintptr_t)dst & 7u)) & 7u;  // bytes before the first aligned word
+  const uint32_t s = 8u * (b & 3u);
+  const bool hi = b >= 4u;
+  const uint32_t w[8] = {o[0], o[1], o[2], o[3], o[4], o[5], n0, n1};
+  uint32_t t[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) t[i] = hi ? w[i + 1] : w[i];
+  uint32_t v[6];  // v[i] = stream bytes [4i + b, 4i + b + 4)
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = __funnelshift_r(t[i], t[i + 1], s);
+  uint2* d = reinterpret_cast<uint2*>(dst + b);
+  d[0] = make_uint2(v[0], v[1]);
+  d[1] = make_uint2(v[2], v[3]);
+  if (b == 0u || has_next) {
+    d[2] = make_uint2(v[4], v[5]);
+  } else {  // own bytes [b + 16, 24) of the straddling word: 8 - b bytes at an aligned address
+    uint8_t* q = dst + b + 16u;
+    const uint32_t n = 8u - b;
+    uint64_t x = (uint64_t)v[5] << 32 | v[4];
+    if (n & 4u) { *reinterpret_cast<uint32_t*>(q) = (uint32_t)x; q += 4; x >>= 32; }
+    if (n & 2u) { *reinterpret_cast<uint16_t*>(q) = (uint16_t)x; q += 2; x >>= 16; }
+    if (n & 1u) *q = (uint8_t)x;
   }
-  const uint64_t X0 = (uint64_t)o[1] << 32 | o[0], X1 = (uint64_t)o[3] << 32 | o[2],
-                 X2 = (uint64_t)o[5] << 32 | o[4];
-  const uint32_t sr = 8u * (8u - a), sl = 8u * a;
-  uint64_t* d = reinterpret_cast<uint64_t*>(dst + (8u - a));  // first aligned word start in this chunk
-  d[0] = (X0 >> sr) | (X1 << sl);
-  d[1] = (X1 >> sr) | (X2 << sl);
-  if (has_next) {
-    const uint64_t N = (uint64_t)n1 << 32 | n0;
-    d[2] = (X2 >> sr) | (N << sl);
-  } else {
-    st_bytes(dst + 24u - a, X2 >> sr, a);  // this chunk's last a bytes
+  if (!has_prev && b) {  // bytes [0, b) before the first aligned word, in aligned pieces
+    uint8_t* q = dst;
+    uint64_t x = (uint64_t)o[1] << 32 | o[0];
+    if ((uintptr_t)q & 1u) { *q = (uint8_t)x; q += 1; x >>= 8; }
+    if ((uintptr_t)q & 2u) { *reinterpret_cast<uint16_t*>(q) = (uint16_t)x; q += 2; x >>= 16; }
+    if ((uintptr_t)q & 4u) *reinterpret_cast<uint32_t*>(q) = (uint32_t)x;
   }
-  if (!has_prev) st_bytes(dst, X0, 8u - a);  // the bytes before the first aligned word
 }
 
 // ---------------------------------------------------------------------------
@@ -432,7 +450,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         // the row-pair tiling of a kVarGen frame puts it mid-granule (frames are 16-aligned)
         const uint64_t a0 = (fbase + off) & ~15ull;
         const uint32_t bytes = (uint32_t)(((fbase + off + len + 15) & ~15ull) - a0);
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        if (p.prod_sleep) mbar_wait_sleep(empty0 + 8 * s, ph ^ 1, p.prod_sleep);
+        else mbar_wait(empty0 + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * s, bytes);
         tma_load_1d(L.slot(s), reinterpret_cast<const void*>(a0), bytes, full0 + 8 * s);
         if (++s == L.stages) { s = 0; ph ^= 1; }
@@ -564,6 +583,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // row-pair tiling constants of the downsample modes (unused otherwise)
   struct {
     uint32_t rowb, upr, dq, dr, last_rows, tin, tob;
+    uint32_t hq, hr, hdq, hdr, oq, orr, odq, odr;  // kVarGen tails: divmod(ctid, tin / tob), divmod(threads, ...)
     int64_t pitch, ow3, tile_out;
     uint8_t* ds_frame;
   } rg{};
@@ -583,6 +603,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     rg.tile_out = (int64_t)(p.rows_per_tile / 2) * rg.pitch;
     rg.tin = ((uint32_t)p.width - 16u * rg.upr) * 3u;          // tail input bytes per row
     rg.tob = ((uint32_t)p.width / 2u - 8u * rg.upr) * 3u;      // tail output bytes per output row
+    if (rg.tin) {
+      rg.hq = (uint32_t)ctid / rg.tin, rg.hr = (uint32_t)ctid - rg.hq * rg.tin;
+      rg.hdq = (uint32_t)kConsThreads / rg.tin, rg.hdr = (uint32_t)kConsThreads - rg.hdq * rg.tin;
+    }
+    if (rg.tob) {
+      rg.oq = (uint32_t)ctid / rg.tob, rg.orr = (uint32_t)ctid - rg.oq * rg.tob;
+      rg.odq = (uint32_t)kConsThreads / rg.tob, rg.odr = (uint32_t)kConsThreads - rg.odq * rg.tob;
+    }
   }
   int64_t item = t0 / p.tpf;
   int32_t k = (int32_t)(t0 - item * p.tpf);
@@ -665,16 +693,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       if constexpr (kGen) {
         // W mod 16 tail pixels of each row, bytewise
         if (rg.tin) {
+          // items t = ctid + i * kConsThreads as (row, byte) pairs advanced without division
           if constexpr (MODE == kModeFused) {  // histogram of every tail byte, all rows of the tile
-            for (uint32_t t = (uint32_t)ctid; t < rows * rg.tin; t += kConsThreads) {
-              const uint32_t r = t / rg.tin, j = t - r * rg.tin;
+            for (uint32_t r = rg.hq, j = rg.hr; r < rows; r += rg.hdq, j += rg.hdr, (j >= rg.tin) ? (j -= rg.tin, ++r) : 0) {
               const uint32_t v = lds_u8(slot + r * rg.rowb + 48u * rg.upr + j);
               atomicAdd(&hsum[(j % 3u) * 16u + (v >> 4)], 1u);
             }
           }
-          if (dsf) {
-            for (uint32_t t = (uint32_t)ctid; t < (rows / 2) * rg.tob; t += kConsThreads) {
-              const uint32_t y = t / rg.tob, j = t - y * rg.tob;
+          if (dsf && rg.tob) {
+            for (uint32_t y = rg.oq, j = rg.orr; y < rows / 2; y += rg.odq, j += rg.odr, (j >= rg.tob) ? (j -= rg.tob, ++y) : 0) {
               const uint32_t i0 = slot + 2u * y * rg.rowb + 48u * rg.upr + 2u * (j - j % 3u) + j % 3u;
               const uint32_t sum = lds_u8(i0) + lds_u8(i0 + 3) + lds_u8(i0 + rg.rowb) + lds_u8(i0 + rg.rowb + 3);
               dsf[(int64_t)y * rg.pitch + 24 * rg.upr + j] = (uint8_t)((sum + 2u) >> 2);
@@ -848,6 +875,9 @@ struct Knobs {
   int max_stages = kDefaultStages;  // SCN_MAX_STAGES: ring-depth cap
   int l2_prefetch_fused = 1;  // SCN_L2_PREFETCH: bulk L2 prefetch distance of the row-pair kernels
   int l2_prefetch_hist = 0;   //   (the read-only histogram keeps 0: the data would cross L2 twice)
+  uint32_t prod_sleep = 0;    // SCN_PROD_SLEEP: producer empty-slot wait suspend hint in ns (0 = spin)
+  int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
+                              // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
 static Knobs g_knobs;
 #ifdef SCN_TUNING
@@ -867,6 +897,8 @@ static void read_knobs_once() {
   k.max_stages = st >= 2 ? st : kDefaultStages;
   const int pf = env_int("SCN_L2_PREFETCH", -1);
   if (pf >= 0) k.l2_prefetch_fused = k.l2_prefetch_hist = pf;
+  k.prod_sleep = (uint32_t)env_int("SCN_PROD_SLEEP", 0);
+  k.gen_warps = env_int("SCN_GEN_WARPS", 0);
   g_knobs = k;
 }
 static const Knobs& knobs() {
@@ -913,6 +945,19 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   if (grid < 1) return cudaSuccess;
   fn<<<grid, NW * 32 + 32, p.smem_bytes, st>>>(p);
   return cudaGetLastError();
+}
+
+// The kVarGen kernels (any width / output alignment) at the knob's warp count.
+template <int MODE>
+static cudaError_t launch_gen(const HistParams& p, cudaStream_t st) {
+  constexpr int kW = MODE == kModeDs ? kGenDsWarps : kGenFusedWarps;
+#ifdef SCN_TUNING
+  const int w = knobs().gen_warps;
+  if (w == 8 && kW != 8) return launch_tma<MODE, 8, kVarGen>(p, st);
+  if (w == 12 && kW != 12) return launch_tma<MODE, 12, kVarGen>(p, st);
+  if (w == 16 && kW != 16) return launch_tma<MODE, 16, kVarGen>(p, st);
+#endif
+  return launch_tma<MODE, kW, kVarGen>(p, st);
 }
 
 // Rows per row-pair tile of the downsample-only kernel: the largest even row count whose
@@ -974,6 +1019,7 @@ static HistParams base_params(const HistJob& j) {
   p.bins = j.bins;
   p.smem_bytes = (uint32_t)g_smem_optin;
   p.max_stages = knobs().max_stages;
+  p.prod_sleep = knobs().prod_sleep;
   p.n_dest = j.n_dest;
   for (int g = 0; g < kMaxDest; ++g) p.dest[g] = j.dest[g];
   return p;
@@ -1053,7 +1099,7 @@ cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int
   p.l2_prefetch = 0;  // measured: the downsample-only kernel keeps 0
   p.table_bytes = 0;
   p.table_align = 128;
-  return gen ? launch_tma<kModeDs, kDsWarps, kVarGen>(p, st) : launch_tma<kModeDs, kDsWarps>(p, st);
+  return gen ? launch_gen<kModeDs>(p, st) : launch_tma<kModeDs, kDsWarps>(p, st);
 }
 
 cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launches) {
@@ -1081,7 +1127,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   p.table_bytes = kTab2Bytes + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
-  return gen ? launch_tma<kModeFused, kDsWarps, kVarGen>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
+  return gen ? launch_gen<kModeFused>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
 }
 
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,

@@ -28,6 +28,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same wait with a suspend-time hint: the thread sleeps in the barrier unit until the
+// phase completes or `ns` pass, instead of spinning issue slots away
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SCN_WAITS_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra SCN_WAITS_%=;\n}\n" ::"r"(bar),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
 // global -> shared 1-D bulk copy, completion signalled on the mbarrier (complete_tx).
 // dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
