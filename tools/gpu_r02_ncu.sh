@@ -3,7 +3,7 @@
 # shape, full-set captures for roofline.traffic (with the library's git SHA), and the launch
 # list of the default bench command. Summaries land in gpurun_out/r02/ncu/.
 set -u
-O=gpurun_out/r02/ncu
+O=${NCU_OUT:-gpurun_out/r02/ncu}
 mkdir -p $O
 SHA=$(python -c "import paper_1805_07339_b200 as s; print(s.scn_version().split(', ')[1].rstrip(')'))")
 echo "library sha $SHA"
@@ -50,3 +50,16 @@ python tools/ncu_traffic.py $O/full_histds.ncu-rep histds 1024 6220800 $SHA $O/n
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --frames 4096 > $O/launches_bench.log 2>&1; echo "launches $?"
 ls -la $O
+for s in 1366x768 854x480; do
+  run histds_gen_$s 1024 C4 histds 0 $s 0
+  run ds_gen_$s 1024 C4 ds 0 $s 0
+done
+# traffic summaries for the other configs' frame sizes (C3 640x360 hist, C5 4K fused)
+timeout 900 ncu --set full --clock-control none -k regex:hist_tma_kernel -s 3 -c 1 -o $O/full_hist_c3 \
+  python tools/hist_tune.py shots 8192 C3 hist --reps 1 > $O/full_hist_c3.log 2>&1; echo "full hist c3 $?"
+python tools/ncu_traffic.py $O/full_hist_c3.ncu-rep hist 8192 691200 $SHA $O/ncu_hist_c3_summary.json \
+  "hist_tma_kernel<0,16>, C3 shape 640x360, 8192 frames/launch"
+timeout 900 ncu --set full --clock-control none -k regex:hist_tma_kernel -s 3 -c 1 -o $O/full_histds_4k \
+  python tools/hist_tune.py shots 512 C5 histds --reps 1 > $O/full_histds_4k.log 2>&1; echo "full histds 4k $?"
+python tools/ncu_traffic.py $O/full_histds_4k.ncu-rep histds 512 24883200 $SHA $O/ncu_histds_4k_summary.json \
+  "hist_tma_kernel<2,8> fused hist+downsample, C5 shape 3840x2160, 512 frames/launch"

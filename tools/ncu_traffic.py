@@ -26,7 +26,7 @@ def main():
         v = float(vals[i].replace(",", ""))
         u = units[i]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(u, 1)
+                 "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "second": 1.0}[u]
         return v * scale
 
     rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
