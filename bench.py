@@ -554,7 +554,9 @@ def run_b200(args):
                     continue
                 g = torch.cuda.CUDAGraph()
                 launches[0] = 0
-                with torch.cuda.graph(g, stream=stream):
+                # thread_local: only this thread's unsafe calls abort the capture (NCCL's
+                # watchdog thread keeps polling its events while we capture)
+                with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
                     fn()
                 graphs[name] = g
                 if name == "step":

@@ -876,6 +876,7 @@ struct Knobs {
   int l2_prefetch_fused = 1;  // SCN_L2_PREFETCH: bulk L2 prefetch distance of the row-pair kernels
   int l2_prefetch_hist = 0;   //   (the read-only histogram keeps 0: the data would cross L2 twice)
   uint32_t prod_sleep = 0;    // SCN_PROD_SLEEP: producer empty-slot wait suspend hint in ns (0 = spin)
+  int hist_warps = 0;         // SCN_HIST_WARPS: consumer warps of the hist-only kernels (tuning build: 8/20)
   int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
                               // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
@@ -899,6 +900,7 @@ static void read_knobs_once() {
   if (pf >= 0) k.l2_prefetch_fused = k.l2_prefetch_hist = pf;
   k.prod_sleep = (uint32_t)env_int("SCN_PROD_SLEEP", 0);
   k.gen_warps = env_int("SCN_GEN_WARPS", 0);
+  k.hist_warps = env_int("SCN_HIST_WARPS", 0);
   g_knobs = k;
 }
 static const Knobs& knobs() {
@@ -1050,11 +1052,19 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
       default:
         p.table_bytes = 3u * 256u * 128u;  // 64 KB PRMT block (channels 0/1) + 32 KB channel 2
         p.table_align = 65536u;
+#ifdef SCN_TUNING
+        if (knobs().hist_warps == 8) return launch_tma<kModePair, 8>(p, st);
+        if (knobs().hist_warps == 20) return launch_tma<kModePair, 20>(p, st);
+#endif
         return launch_tma<kModePair, kHistWarps>(p, st);
     }
   }
   p.table_bytes = 3u * 256u * 128u;
   p.table_align = 65536u;
+#ifdef SCN_TUNING
+  if (knobs().hist_warps == 8) return launch_tma<kModeRaw, 8>(p, st);
+  if (knobs().hist_warps == 20) return launch_tma<kModeRaw, 20>(p, st);
+#endif
   return launch_tma<kModeRaw, kHistWarps>(p, st);
 }
 
