@@ -3,7 +3,9 @@
 #   make oracle     -> CPU oracle only (gcc)
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-GIT_SHA   := $(shell git rev-parse --short=12 HEAD 2>/dev/null || echo unknown)
+# the library's version = the last commit that changed its sources (doc-only commits keep it,
+# so ncu captures of the same kernels stay matched to the library, bench.py traffic_source)
+GIT_SHA   := $(shell git log -1 --format=%h --abbrev=12 -- paper_1805_07339_b200/csrc include Makefile 2>/dev/null | grep . || echo unknown)
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -shared -cudart static
 CC        ?= gcc
 CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra -shared
@@ -33,10 +35,10 @@ oracle: $(ORACLE) $(SYNTH_HOST)
 micro: $(MICRO)
 
 # .git/logs/HEAD changes with every commit, so the embedded SHA (scn_version) stays current
-$(LIB): $(LIB_SRCS) $(LIB_HDRS) $(wildcard .git/logs/HEAD)
+$(LIB): $(LIB_SRCS) $(LIB_HDRS) Makefile $(wildcard .git/logs/HEAD)
 	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_GIT_SHA=\"$(GIT_SHA)\" -Xptxas -v $(LIB_SRCS) -o $@ 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
 
-$(LIB_TUNE): $(LIB_SRCS) $(LIB_HDRS) $(wildcard .git/logs/HEAD)
+$(LIB_TUNE): $(LIB_SRCS) $(LIB_HDRS) Makefile $(wildcard .git/logs/HEAD)
 	$(NVCC) $(NVFLAGS) -Iinclude -DSCN_TUNING -DSCN_GIT_SHA=\"$(GIT_SHA)-tuning\" $(LIB_SRCS) -o $@
 
 $(SYNTH_HOST): scn_synth/synth_host.c scn_synth/scn_synth.h
