@@ -1,7 +1,7 @@
 #!/bin/bash
 # r02 round pass on one B200: tests, smoke, every bench line, reference arm, ncu evidence.
 # Everything lands in gpurun_out/r02/round/ (copied to profiles/ by hand).
-O=gpurun_out/r02/round
+O=${ROUND_OUT:-gpurun_out/r02/round}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit,driver_version --format=csv > $O/box.txt
 nproc >> $O/box.txt; lscpu | grep "Model name" >> $O/box.txt
@@ -30,3 +30,5 @@ for impl in 1 2; do $B --hist-impl $impl --frames 1024 --steps 5 --no-cpu-baseli
 for g in nccl p2p; do timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr=127.0.0.1 --master-port=$((20000 + RANDOM % 20000)) bench.py --gpus 2 --dist-backend gloo --gather $g --no-e2e --no-cpu-baseline --steps 10 > $O/bench_n2_shared_gpu_$g.json 2>$O/bench_n2_shared_gpu_$g.err; echo "n2 $g $?"; done
 $B --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2>/dev/null; echo "ref $?"
 NCU_OUT=$O/ncu bash tools/gpu_r02_ncu.sh > $O/ncu_pass.log 2>&1; echo "ncu $?"
+T="python tools/hist_tune.py shots"
+for r in 1 2; do for sh in 1366x768 854x480 426x240; do for op in histds ds; do $T 2048 C4 $op --shape $sh >> $O/tune_gen.jsonl 2>/dev/null; done; done; done
