@@ -249,3 +249,19 @@ def test_fused_gather_local_destinations():
         np.testing.assert_array_equal(_u32(d), D)
     with pytest.raises(scn.ScnError):
         scn.scn_run_hist_shotdiff_to(job.seq, 0, 1, 16, [], [], 0, scratch)
+
+
+@pytest.mark.parametrize("bins", [2, 3, 8, 17, 100, 128, 255])
+@pytest.mark.parametrize("mode", ["uniform", "shots"])
+def test_every_bin_kernel_path(bins, mode):
+    # bins dividing 16 merge 16-level pair-key bins at the flush; every other B counts raw values
+    # and maps them to bins at the flush (K2r) — uniform content reaches every bin edge
+    wl = Workload("bins", 211, 37, 2, 12, ("stride", 1), ("hist", "shotdiff"), bins=bins,
+                  spec_kw={"len_min": 2, "len_max": 5})
+    v, r, s = _oracle_positions(wl)
+    spec = wl.spec(mode=mode)
+    H, D, _ = oracle.run(spec, v, r, s, 0, len(r), bins)
+    got = _run(wl, 0, len(r), ("hist", "shotdiff"), bins, spec=spec)
+    np.testing.assert_array_equal(got["hist"], H)
+    np.testing.assert_array_equal(got["diff"], D)
+    assert scn.scn_hist_variant(bins) == ("tma_pair_lane_private" if 16 % bins == 0 else "tma_raw_lane_private_remap")
