@@ -324,6 +324,18 @@ __device__ __forceinline__ void st_global_24(uint8_t* dst, const uint32_t* o) { 
   d[1] = make_uint2(o[2], o[3]);
   d[2] = make_uint2(o[4], o[5]);
 }
+__device__ __forceinline__ void st_pred_u8(uint8_t* p, uint32_t v, bool pr) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.u8 [%0], %1; }" ::"l"(p), "r"(v),
+               "r"((uint32_t)pr) : "memory");
+}
+__device__ __forceinline__ void st_pred_u16(uint8_t* p, uint32_t v, bool pr) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.u16 [%0], %1; }" ::"l"(p), "r"(v),
+               "r"((uint32_t)pr) : "memory");
+}
+__device__ __forceinline__ void st_pred_u32(uint8_t* p, uint32_t v, bool pr) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.u32 [%0], %1; }" ::"l"(p), "r"(v),
+               "r"((uint32_t)pr) : "memory");
+}
 // 24 output bytes at ANY address (kVarGen). Lanes of one row write consecutive 24-byte
 // chunks; each lane stores the three aligned 8-byte words that START inside its chunk —
 // when the chunk is not 8-aligned the third one ends in the next lane's chunk, whose first
@@ -349,23 +361,24 @@ __device__ __forceinline__ void st_global_24_any(uint8_t* dst, const uint32_t* o
   uint2* d = reinterpret_cast<uint2*>(dst + b);
   d[0] = make_uint2(v[0], v[1]);
   d[1] = make_uint2(v[2], v[3]);
-  if (b == 0u || has_next) {
-    d[2] = make_uint2(v[4], v[5]);
-  } else {  // own bytes [b + 16, 24) of the straddling word: 8 - b bytes at an aligned address
-    uint8_t* q = dst + b + 16u;
-    const uint32_t n = 8u - b;
-    uint64_t x = (uint64_t)v[5] << 32 | v[4];
-    if (n & 4u) { *reinterpret_cast<uint32_t*>(q) = (uint32_t)x; q += 4; x >>= 32; }
-    if (n & 2u) { *reinterpret_cast<uint16_t*>(q) = (uint16_t)x; q += 2; x >>= 16; }
-    if (n & 1u) *q = (uint8_t)x;
-  }
-  if (!has_prev && b) {  // bytes [0, b) before the first aligned word, in aligned pieces
-    uint8_t* q = dst;
-    uint64_t x = (uint64_t)o[1] << 32 | o[0];
-    if ((uintptr_t)q & 1u) { *q = (uint8_t)x; q += 1; x >>= 8; }
-    if ((uintptr_t)q & 2u) { *reinterpret_cast<uint16_t*>(q) = (uint16_t)x; q += 2; x >>= 16; }
-    if ((uintptr_t)q & 4u) *reinterpret_cast<uint32_t*>(q) = (uint32_t)x;
-  }
+  if (b == 0u || has_next) d[2] = make_uint2(v[4], v[5]);
+  // Words without a neighbour, written as naturally aligned 4/2/1-byte pieces by predicated
+  // stores (branch-free: the edge lanes of a warp would otherwise serialise two branches).
+  // Tail: own bytes [b + 16, 24) = n = 8 - b bytes at the aligned q = dst + b + 16.
+  const bool tl = b != 0u && !has_next;
+  const uint32_t n = 8u - b;
+  uint8_t* q = dst + b + 16u;
+  st_pred_u32(q, v[4], tl && (n & 4u));
+  const uint32_t t2 = (n & 4u) ? v[5] : v[4];
+  st_pred_u16(q + (n & 4u), t2, tl && (n & 2u));
+  st_pred_u8(q + (n & 6u), t2 >> (8u * (n & 2u)), tl && (n & 1u));
+  // Head: bytes [0, b) at dst (alignment a = 8 - b): a 1-byte piece up to 2-alignment, a
+  // 2-byte piece up to 4-alignment, a 4-byte piece up to the first aligned word.
+  const bool hd = b != 0u && !has_prev;
+  const uint32_t a = 8u - b, a1 = a + (a & 1u), a2 = a1 + (a1 & 2u);
+  st_pred_u8(dst, o[0], hd && (a & 1u));
+  st_pred_u16(dst + (a1 - a), __funnelshift_r(o[0], o[1], 8u * (a1 - a)), hd && (a1 & 2u));
+  st_pred_u32(dst + (a2 - a), __funnelshift_r(o[0], o[1], 8u * (a2 - a)), hd && (a2 & 4u));
 }
 
 // ---------------------------------------------------------------------------
