@@ -52,8 +52,36 @@ def main():
     # fused split layout with several row-pair tiles per frame (24-row tiles, 4-row tail)
     w3 = Workload("san3", 640, 100, 1, 6, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 4})
     check(w3, ("hist", "downsample"), 16)
+    # realigning row-pair kernels (kVarGen): odd widths, several tiles per frame, odd output offsets
+    check(w2, ("hist", "downsample"), 16)
+    w4 = Workload("san4", 854, 30, 1, 4, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 4})
+    check(w4, ("hist", "downsample"), 16)
+    check(w4, ("downsample",), 16, fused=False)
+    unaligned_out(w4)
+    # the north_star's K2a and K2a' (per-warp bins, __match_any_sync)
+    import paper_1805_07339_b200 as scn
+    for impl in (1, 2):
+        scn.scn_set_hist_impl(impl)
+        check(w1, ("hist", "shotdiff"), 16)
+    scn.scn_set_hist_impl(0)
     next_rows()
     print("sanitize_run ok")
+
+
+def unaligned_out(wl):
+    import paper_1805_07339_b200 as scn
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    job = scn_harness.DeviceJob(wl, 0, M, with_halo=False, plan_=pl)
+    _, _, DS = oracle.run(wl.spec(), pl[0], pl[1], pl[2], 0, M, 16, want_ds=True)
+    nb = M * (wl.height // 2) * (wl.width // 2) * 3
+    buf = torch.zeros(nb + 16, dtype=torch.uint8, device="cuda")
+    hist = torch.empty((M, 3, 16), dtype=torch.int32, device="cuda")
+    scn.scn_run_hist_downsample(job.seq, 0, M, 16, hist, buf.data_ptr() + 3, job.stream)
+    scn.scn_run_downsample(job.seq, 0, M, buf.data_ptr() + 3, job.stream)
+    torch.cuda.synchronize()
+    assert (buf.cpu().numpy()[3:3 + nb] == DS.reshape(-1)).all()
+    job.close()
 
 
 def next_rows():
