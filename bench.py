@@ -106,9 +106,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
 
-    def stop(self):
+    def stop(self, window=None):
+        """Clock statistics over the samples taken inside `window` = (t0, t1) wall seconds (the
+        timed region; all samples if the region was too short to catch one)."""
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -119,7 +121,11 @@ class ClockSampler:
             self.thread.join(timeout=2)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, mx, reasons = [], [], set()
-        for s in self.samples:
+        picked = [p for t, p in self.samples if window is None or window[0] <= t <= window[1] + 0.15]
+        in_window = bool(picked) and window is not None
+        if not picked:
+            picked = [p for _, p in self.samples]
+        for s in picked:
             try:
                 sm.append(float(s[0]))
                 mx.append(float(s[1]))
@@ -129,7 +135,8 @@ class ClockSampler:
                 if s[3 + i].lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "timed region" if in_window else "whole sampling run (timed region shorter than a sample)"}
 
 
 def traffic_from_profile(frames: int, F: int, kernel: str, lib_version: str):
@@ -599,8 +606,9 @@ def run_b200(args):
     clocks = ClockSampler(gpu_id)
     clocks.start()
     time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
+    w0 = time.time()
     step_ms = timed(run["step"], args.steps)  # the timed region: barrier + sync on both sides
-    clk = clocks.stop()
+    clk = clocks.stop((w0, time.time()))
     gpu_launches = per_step_launches * args.steps if use_graph else launches[0]
     total_ms = float(sum(step_ms))
     # breakdown (after the timed region): the compute and the exchange alone, same K
