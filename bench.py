@@ -64,6 +64,8 @@ def parse():
                          "(the config's input N times over)")
     ap.add_argument("--shape", default="", help="override the config's frame size, WxH (e.g. 1366x768)")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--force-graph", action="store_true",
+                    help="try graph capture even with gloo (test of the capture-failure fallback)")
     ap.add_argument("--hist-impl", type=int, default=0,
                     help="scn_set_hist_impl: 0 lane-private pair keys (default), 1 K2a match per byte, 2 K2a' packed")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
@@ -552,7 +554,7 @@ def run_b200(args):
     # One CUDA graph per rank for the step (memset + histogram + shot-diff + all-gather), and
     # two more for the breakdown (compute only, exchange only). gloo collectives run on the
     # host and cannot be captured, so a gloo run (N > 1 ranks sharing one GPU) stays eager.
-    use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl")
+    use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl" or args.force_graph)
     graphs, per_step_launches, graph_note = {}, 0, None
     if use_graph:
         try:
