@@ -554,7 +554,9 @@ def run_b200(args):
     # One CUDA graph per rank for the step (memset + histogram + shot-diff + all-gather), and
     # two more for the breakdown (compute only, exchange only). gloo collectives run on the
     # host and cannot be captured, so a gloo run (N > 1 ranks sharing one GPU) stays eager.
-    use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl" or args.force_graph)
+    # (the fused peer gather has no collective in the step, so it captures under any backend)
+    use_graph = not args.no_graph and (world == 1 or args.dist_backend == "nccl" or peer is not None or
+                                       args.force_graph)
     graphs, per_step_launches, graph_note = {}, 0, None
     if use_graph:
         try:
