@@ -51,8 +51,11 @@ def parse():
     ap.add_argument("--round-frames", type=int, default=0,
                     help="process a rank's shard in rounds of this many positions (input + output > HBM, e.g. C5 "
                          "at N = 1); generation between rounds is untimed, timed steps are summed over rounds")
-    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1 result exchange: NCCL all_gather (default) or fused into the kernels over peer memory")
+    ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N > 1 result exchange: p2p = fused into the histogram / shot-diff kernels over peer "
+                         "memory (scn_run_hist_shotdiff_to); nccl = one NCCL all_gather of the result block; "
+                         "auto (default) = p2p for the hist + shot-diff step (NCCL if a rank cannot map its "
+                         "peers), nccl for the other ops")
     ap.add_argument("--cuts", type=int, default=0,
                     help="NEXT N3: add the bounded-state adaptive cut detector with warmup W to the step")
     ap.add_argument("--bins", type=int, default=0, help="override the config's bins per channel (NEXT N4: 256)")
@@ -492,10 +495,11 @@ def run_b200(args):
     do_diff, do_ds = "shotdiff" in wl.ops, "downsample" in wl.ops
     ops = tuple(o for o in ("hist", "shotdiff", "downsample") if o == "hist" or o in wl.ops)
     out = job.alloc_outputs(ops, bins)
-    p2p = world > 1 and args.gather == "p2p"
-    gather_note = None
-    if p2p and (do_ds or cut_w or not do_diff):
+    fusable = do_diff and not do_ds and not cut_w  # the step scn_run_hist_shotdiff_to covers
+    if args.gather == "p2p" and not fusable:
         raise SystemExit("--gather p2p covers the hist + shot-diff step only")
+    p2p = world > 1 and (args.gather == "p2p" or (args.gather == "auto" and fusable))
+    gather_note = None
     peer = None
     if p2p:  # the fused peer-memory gather, or NCCL if any rank cannot map its peers' columns
         err = None

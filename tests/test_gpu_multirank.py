@@ -66,7 +66,7 @@ def test_nccl_one_rank_per_gpu():
     assert r.stdout.count("PASS") == world
 
 
-@pytest.mark.parametrize("gather", ["nccl", "p2p"])
+@pytest.mark.parametrize("gather", ["nccl", "p2p", "auto"])
 def test_bench_two_ranks_strong_scaling(gather):
     # bench.py at N = 2 (strong scaling of a C2 prefix; NCCL + CUDA graphs on a >= 2-GPU box,
     # two ranks sharing the GPU over gloo otherwise) prints one line covering all frames
@@ -79,3 +79,5 @@ def test_bench_two_ranks_strong_scaling(gather):
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["config"]["frames"] == 256 and line["config"]["frames_per_gpu"] == 128
     assert len(line["breakdown"]["compute_ms"]) == 2 and line["gpu_launches"] > 0
+    # auto = the fused peer-memory gather for the hist + shot-diff step
+    assert line["config"]["ops"].endswith("+nccl_allgather" if gather == "nccl" else "+fused_peer_gather")
