@@ -511,7 +511,8 @@ def run_b200(args):
         dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if float(bad[0]):
             if peer is not None:
-                peer.close()
+                peer.close(barrier=False)
+            dist.barrier()  # every rank, mapped or not, before the columns are dropped
             peer, p2p = None, False
             gather_note = "p2p unavailable, fell back to NCCL all_gather: " + (err or "failed on another rank")
     gather = scn_harness.ColumnGather(M, world, bins, dev, dist) if world > 1 and peer is None else None

@@ -399,8 +399,17 @@ class PeerColumns:
                 raise RuntimeError(f"unexpected CUDA IPC handle length {len(handle)}")
             return handle, int(off) + t.storage_offset() * t.element_size()
 
+        # every rank joins the exchange even if its own export fails, so a failure on one rank
+        # cannot leave the others waiting in the collective
+        try:
+            mine, err = (export(self.hist), export(self.diff)), None
+        except Exception as ex:  # noqa: BLE001 (re-raised on every rank below)
+            mine, err = None, f"{type(ex).__name__}: {ex}"
         objs = [None] * self.world
-        dist.all_gather_object(objs, (export(self.hist), export(self.diff)))
+        dist.all_gather_object(objs, mine)
+        self.bases = None
+        if any(o is None for o in objs):
+            raise RuntimeError(err or "a peer could not export its result columns")
         self.bases = []
         self.hist_ptrs, self.diff_ptrs = [], []
         for g, ((hh, ho), (dh, do)) in enumerate(objs):
@@ -418,11 +427,14 @@ class PeerColumns:
             self.hist_ptrs.append(ph)
             self.diff_ptrs.append(pd)
 
-    def close(self):
+    def close(self, barrier: bool = True):
+        """Release the peer mappings; with barrier (every rank must call it then), peers drop
+        their mappings before owners free the columns."""
         if self.bases is None:
             return
         torch.cuda.synchronize()
         for b in self.bases:
             scn.scn_ipc_release(b)
         self.bases = None
-        self.dist.barrier()  # peers drop their mappings before owners free
+        if barrier:
+            self.dist.barrier()
