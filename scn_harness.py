@@ -10,6 +10,8 @@ only by the callers that are allowed to use it (tests, smoke, bench baseline).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -402,6 +404,8 @@ class PeerColumns:
         # every rank joins the exchange even if its own export fails, so a failure on one rank
         # cannot leave the others waiting in the collective
         try:
+            if os.environ.get("SCN_TEST_P2P_FAIL_RANK") == str(self.rank):  # test hook: the fallback path
+                raise RuntimeError("export disabled by SCN_TEST_P2P_FAIL_RANK")
             mine, err = (export(self.hist), export(self.diff)), None
         except Exception as ex:  # noqa: BLE001 (re-raised on every rank below)
             mine, err = None, f"{type(ex).__name__}: {ex}"

@@ -81,3 +81,15 @@ def test_bench_two_ranks_strong_scaling(gather):
     assert len(line["breakdown"]["compute_ms"]) == 2 and line["gpu_launches"] > 0
     # auto = the fused peer-memory gather for the hist + shot-diff step
     assert line["config"]["ops"].endswith("+nccl_allgather" if gather == "nccl" else "+fused_peer_gather")
+
+
+def test_bench_p2p_fallback_to_allgather():
+    # one rank cannot export its columns: every rank falls back to the all-gather, no hang
+    import json
+    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
+    r = _torchrun(2, ("bench.py",), "--gpus", "2", "--steps", "3", "--warmup", "3", "--frames", "256",
+                  "--no-e2e", "--no-cpu-baseline", "--dist-backend", backend, env={"SCN_TEST_P2P_FAIL_RANK": "1"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["config"]["ops"].endswith("+nccl_allgather")
+    assert "fell back" in line["config"]["gather_note"]
