@@ -2,6 +2,8 @@
 whose rows straddle tiles), bin counts, sampling kinds, table counts, content modes,
 shard counts and op combinations, each compared bit-exactly with the oracle. Every case
 is derived from its index, so a failure names a reproducible case."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -41,7 +43,10 @@ def _case(i):
     return w, h, n_videos, rows, sampling, bins, mode, ops, G
 
 
-@pytest.mark.parametrize("i", range(160))
+N_CASES = int(os.environ.get("SCN_FUZZ_CASES", "160"))  # e.g. 2000 for a long sweep
+
+
+@pytest.mark.parametrize("i", range(N_CASES))
 def test_fuzz_case(i):
     w, h, n_videos, rows, sampling, bins, mode, ops, G = _case(i)
     wl = Workload(f"fuzz{i}", w, h, n_videos, rows, sampling, ops, bins=bins, spec_kw={"len_min": 2, "len_max": 6})
@@ -56,6 +61,11 @@ def test_fuzz_case(i):
             continue
         job = scn_harness.DeviceJob(wl, b, e, with_halo="shotdiff" in ops, spec=spec, plan_=pl)
         out = job.alloc_outputs(ops, bins)
+        if "downsample" in ops and i % 3 == 1:  # an output buffer at an odd byte offset
+            nb = out["ds"].numel()
+            raw = torch.empty(nb + 8, dtype=torch.uint8, device=out["ds"].device)
+            off = 1 + i % 7
+            out["ds"] = raw[off:off + nb].view(out["ds"].shape)
         job.run(out, ops, bins)
         torch.cuda.synchronize()
         n = e - b
