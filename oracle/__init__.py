@@ -44,6 +44,10 @@ def lib():
                                           ctypes.c_int64, i64p]
         L.oracle_sample_gather.argtypes = [ctypes.c_int64, i64p, ctypes.c_int64, i64p, ctypes.c_int64, i64p]
         L.oracle_hist.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        L.oracle_hist_joint.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_void_p]
+        L.oracle_run_joint.argtypes = [ctypes.POINTER(scn_synth.SynthSpecC), ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
         L.oracle_shotdiff.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.c_void_p]
         L.oracle_downsample.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
@@ -114,6 +118,31 @@ def hist(frame: np.ndarray, bins: int = 16) -> np.ndarray:
     if rc:
         raise OracleError(rc, "hist")
     return out
+
+
+def hist_joint(frame: np.ndarray, j: int = 4) -> np.ndarray:
+    """NEXT N4 joint-colour histogram of one HWC RGB8 frame -> uint32 [J^3],
+    k = bin(R)*J*J + bin(G)*J + bin(B), bin(v) = floor(v*J/256)."""
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    h, w, c = f.shape
+    assert c == 3
+    out = np.zeros(j ** 3, dtype=np.uint32)
+    rc = lib().oracle_hist_joint(_ptr(f), w, h, j, _ptr(out))
+    if rc:
+        raise OracleError(rc, "hist_joint")
+    return out
+
+
+def run_joint(spec: "scn_synth.Spec", videos, rows, p0: int, p1: int, j: int = 4) -> np.ndarray:
+    """Joint-colour histograms of the synthetic frames at sampled positions [p0, p1) -> [n, J^3]."""
+    v = np.ascontiguousarray(videos, dtype=np.int32)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    n = p1 - p0
+    out = np.zeros((max(n, 1), j ** 3), dtype=np.uint32)
+    rc = lib().oracle_run_joint(ctypes.byref(spec.c), _ptr(v), _ptr(r), p0, p1, j, _ptr(out))
+    if rc:
+        raise OracleError(rc, "run_joint")
+    return out[:n]
 
 
 def shotdiff(hists: np.ndarray, seg_start=None) -> np.ndarray:

@@ -124,6 +124,49 @@ int oracle_hist(const uint8_t* frame, int32_t w, int32_t h, int32_t bins, uint32
 }
 
 /* ------------------------------------------------------------------------
+ * NEXT N4, joint-colour variant (SURVEY §8(f) N4 "256-bin per-channel (or
+ * joint-colour) histogram"; "pixel color histogram", reading Q3's
+ * alternative): one histogram over colour triples, J bins per channel,
+ * bin_J(v) = floor(v*J/256) as in reading Q2, joint bin
+ * k = bin_J(R)*J*J + bin_J(G)*J + bin_J(B), layout out[k], k < J^3.
+ * frame: H rows of W pixels of 3 bytes (HWC), row-major, contiguous.
+ * ------------------------------------------------------------------------ */
+int oracle_hist_joint(const uint8_t* frame, int32_t w, int32_t h, int32_t j, uint32_t* out) {
+  if (j < 1 || j > 16) return OR_EUNSUPPORTED;
+  if (w < 1 || h < 1) return OR_EINVAL;
+  const int32_t n = j * j * j;
+  for (int32_t k = 0; k < n; ++k) out[k] = 0;
+  for (int32_t y = 0; y < h; ++y) {
+    for (int32_t x = 0; x < w; ++x) {
+      const uint8_t* px = frame + ((int64_t)y * w + x) * 3;
+      uint32_t b[3];
+      for (int32_t c = 0; c < 3; ++c) b[c] = ((uint32_t)px[c] * (uint32_t)j) / 256u;  /* floor(v*J/256) */
+      out[(b[0] * (uint32_t)j + b[1]) * (uint32_t)j + b[2]] += 1u;
+    }
+  }
+  return OR_OK;
+}
+
+/* Joint histograms of the synthetic frames at sampled positions [p0, p1)
+ * (the frames oracle_run generates): out [p1-p0][J^3]. */
+int oracle_run_joint(const synth_spec* spec, const int32_t* videos, const int64_t* rows, int64_t p0, int64_t p1,
+                     int32_t j, uint32_t* out) {
+  if (j < 1 || j > 16) return OR_EUNSUPPORTED;
+  if (p0 < 0 || p1 < p0) return OR_EINVAL;
+  const int64_t F = (int64_t)spec->width * spec->height * 3, n = (int64_t)j * j * j;
+  uint8_t* frame = (uint8_t*)malloc((size_t)(F > 0 ? F : 1));
+  if (!frame) return OR_EINVAL;
+  for (int64_t p = p0; p < p1; ++p) {
+    synth_frame_desc d = synth_describe(spec, videos[p], rows[p]);
+    synth_fill_frame_host(spec, &d, frame);
+    int rc = oracle_hist_joint(frame, spec->width, spec->height, j, out + (p - p0) * n);
+    if (rc) { free(frame); return rc; }
+  }
+  free(frame);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------
  * Shot-diff: a [-1,0] stencil over the SAMPLED sequence ("Stencil
  * operations gain access to a window of elements from the input sequence
  * defined by a constant-offset stencil"; sample-then-stencil composition,
