@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--force-graph", action="store_true",
                     help="try graph capture even with gloo (test of the capture-failure fallback)")
+    ap.add_argument("--joint", type=int, default=0,
+                    help="NEXT N4 joint-colour histogram with J bins per channel (J^3 bins) instead of the "
+                         "config's ops (N = 1)")
     ap.add_argument("--hist-impl", type=int, default=0,
                     help="scn_set_hist_impl: 0 lane-private pair keys (default), 1 K2a match per byte, 2 K2a' packed")
     ap.add_argument("--graph", default="f", choices=["f", "e"],
@@ -351,6 +354,68 @@ def run_montage(args):
                        "ops": "job1 hist+shotdiff -> D2H -> select -> job2 gather+downsample montage"},
             "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
             "step_ms_min": min(ts)}
+    print(json.dumps(line), flush=True)
+    job.close()
+    return 0
+
+
+def run_joint(args):
+    """NEXT N4, joint-colour variant: scn_run_histogram_joint (J bins per channel, J^3 counters
+    per frame) over the config's sampled frames, device-resident, N = 1."""
+    import torch
+
+    import paper_1805_07339_b200 as scn
+    import scn_harness
+    import scn_synth
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = _apply_shape(scn_synth.WORKLOADS[args.config], args)
+    st = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(st)
+    pl = scn_harness.plan(wl)
+    M = len(pl[1]) if args.frames <= 0 else min(args.frames, len(pl[1]))
+    pl = tuple(x[:M] for x in pl)
+    job = scn_harness.DeviceJob(wl, 0, M, with_halo=False, device=dev, stream=st, plan_=pl,
+                                spec=wl.spec(mode=args.mode))
+    J = args.joint
+    out = torch.empty((max(M, 1), J ** 3), dtype=torch.int32, device=dev)
+
+    def step():
+        scn.scn_run_histogram_joint(job.seq, 0, M, J, out, st)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    launches = scn.scn_last_launch_count()
+    torch.cuda.synchronize(dev)
+    props = torch.cuda.get_device_properties(dev)
+    clocks = ClockSampler(f"GPU-{props.uuid}" if getattr(props, "uuid", None) else "0")
+    clocks.start()
+    time.sleep(0.3)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    w0 = time.time()
+    ev[0].record(st)
+    for k in range(args.steps):
+        step()
+        ev[k + 1].record(st)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop((w0, time.time()))
+    ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    step_ms = float(np.mean(ms))
+    peak, peak_src = load_peaks()
+    alg = M * (wl.frame_bytes + J ** 3 * 4)
+    ach = alg / (step_ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": M / (step_ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name + f" joint-colour histogram J={J} (NEXT N4)", "frames": M,
+                       "width": wl.width, "height": wl.height, "joint_bins": J ** 3, "content": args.mode,
+                       "ops": "hist_joint", "l2": "no flush: input %.1f GB >> 126 MB L2" % (M * wl.frame_bytes / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                         "kernel": "hist_tma_kernel<7,16> (scn_run_histogram_joint incl. memset)",
+                         **stream_ceiling(False, ach)},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps, "clocks": clk,
+            "step_ms_min": float(min(ms)), "library": scn.scn_version()}
     print(json.dumps(line), flush=True)
     job.close()
     return 0
@@ -848,6 +913,8 @@ def main():
         return run_graph_e(args)
     if args.montage > 0:
         return run_montage(args)
+    if args.joint > 0:
+        return run_joint(args)
     if args.round_frames > 0 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         return run_rounds(args)
     return run_b200(args)

@@ -147,6 +147,16 @@ void scn_seq_destroy(scn_seq* s);
 scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, uint32_t* d_hist,
                              void* stream);
 
+/* NEXT N4, joint-colour variant (SURVEY §8(f) N4 "256-bin per-channel (or
+ * joint-colour) histogram"; "pixel color histogram", the joint
+ * alternative of reading Q3): d_hist[j][k] (u32, [end-begin][J^3], J =
+ * bins_per_channel) = number of pixels of frame j whose colour (R,G,B) has
+ * k = bin(R)*J*J + bin(G)*J + bin(B), bin(v) = floor(v*J/256) (reading Q2).
+ * d_hist is zeroed by the call. EUNSUPPORTED if J is outside [1,8] (the
+ * lane-private table holds J^3 <= 512 rows). */
+scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
+                                   uint32_t* d_hist, void* stream);
+
 /* Shot-diff ("detect shot boundaries (via histogram differences)") as
  * a [-1,0] stencil over the sampled sequence (fig:sampling-f; reading
  * Q7): d_diff[j] (u32) = sum_c sum_b |H[j][c][b] - H[j-1][c][b]|, and 0 at the

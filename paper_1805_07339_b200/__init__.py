@@ -68,6 +68,7 @@ _sig("scn_seq_device_bytes", _sz, _vp)
 _sig("scn_seq_upload", ctypes.c_int, _vp, _vp, _sz, _vp)
 _sig("scn_seq_destroy", None, _vp)
 _sig("scn_run_histogram", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp)
+_sig("scn_run_histogram_joint", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp)
 _sig("scn_run_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_hist_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_downsample", ctypes.c_int, _vp, _i64, _i64, _vp, _vp)
@@ -230,6 +231,11 @@ def scn_seq_destroy(s) -> None:
 
 def scn_run_histogram(s, begin, end, bins, d_hist, stream=None) -> None:
     _check(_lib.scn_run_histogram(s, begin, end, bins, _ptr(d_hist), _stream(stream)), "scn_run_histogram")
+
+
+def scn_run_histogram_joint(s, begin, end, bins_per_channel, d_hist, stream=None) -> None:
+    _check(_lib.scn_run_histogram_joint(s, begin, end, bins_per_channel, _ptr(d_hist), _stream(stream)),
+           "scn_run_histogram_joint")
 
 
 def scn_run_shotdiff(s, begin, end, bins, d_hist, d_diff, d_scratch=None, stream=None) -> None:

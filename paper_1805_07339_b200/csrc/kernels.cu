@@ -55,7 +55,9 @@
 
 namespace scn {
 
-enum : int { kModePair = 0, kModeFused = 2, kModeDs = 3, kModeRaw = 4, kModeMatch = 5, kModeMatchPacked = 6 };
+enum : int {
+  kModePair = 0, kModeFused = 2, kModeDs = 3, kModeRaw = 4, kModeMatch = 5, kModeMatchPacked = 6, kModeJoint = 7
+};
 constexpr int kVarGen = 1;  // row-pair modes: any width / output alignment
 
 constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 producer warp)
@@ -86,6 +88,7 @@ struct HistParams {
   int32_t ds_cols;   // > 0: montage tiles (NEXT N1)
   int64_t F;
   int32_t width, height, bins;
+  int32_t joint;          // kModeJoint: J bins per channel (the output row holds J^3 counters)
   uint32_t tile;          // frame bytes per full tile (row-pair modes: rows_per_tile * W * 3)
   uint32_t slot;          // shared-memory bytes per ring slot (>= tile; + kGenSlack for kVarGen)
   int32_t rows_per_tile;  // row-pair modes: rows per tile (even); 0 otherwise
@@ -260,6 +263,49 @@ __device__ __forceinline__ void match_packed_word(const uint32_t* w, uint32_t am
   }
 }
 
+// ---- NEXT N4 joint-colour keys: one key per pixel, k = (bR * J + bG) * J + bB ------------
+// Pixel P of a unit is bytes 3P..3P+2; each channel byte is zero-extended by one PRMT and
+// binned as (v * J) >> 8 (reading Q2); the key picks a 128-byte lane-private row.
+template <int P>
+__device__ __forceinline__ uint32_t joint_key(const uint32_t* w, uint32_t J) {
+  constexpr int i0 = 3 * P, i1 = 3 * P + 1, i2 = 3 * P + 2;
+  const uint32_t r = __byte_perm(w[i0 >> 2], 0u, 0x4440u + (i0 & 3));
+  const uint32_t g = __byte_perm(w[i1 >> 2], 0u, 0x4440u + (i1 & 3));
+  const uint32_t b = __byte_perm(w[i2 >> 2], 0u, 0x4440u + (i2 & 3));
+  return (((r * J) >> 8) * J + ((g * J) >> 8)) * J + ((b * J) >> 8);
+}
+template <int... P>
+__device__ __forceinline__ void joint_unit_all(const uint32_t* w, uint32_t lane4, uint32_t J,
+                                               std::integer_sequence<int, P...>) {
+  (red_shared_add_off<0>(lane4 + joint_key<P>(w, J) * 128u), ...);
+}
+__device__ __forceinline__ void hist_unit_joint(const uint32_t* w, uint32_t lane4, uint32_t J) {
+  joint_unit_all(w, lane4, J, std::make_integer_sequence<int, 16>{});
+}
+// J = 2^L: bin(v) = v >> (8 - L), so each channel's bin field is cut from its word by one shift
+// and OR-ed into the row address (table | k << 7 | lane << 2) by one LOP3 with a constant mask:
+// 3 SHF + 3 LOP3 + 1 ATOMS per pixel (the generic path needs 12 ALU/FMA ops per pixel).
+template <int L, int I, int T>
+__device__ __forceinline__ uint32_t joint_field(const uint32_t* w, uint32_t acc) {
+  constexpr int s = 8 * (I & 3) + 8 - L - T;  // bring the byte's top L bits to bit T
+  const uint32_t x = s >= 0 ? (w[I >> 2] >> (s >= 0 ? s : 0)) : (w[I >> 2] << (s < 0 ? -s : 0));
+  return lop3_and_or<((1u << L) - 1u) << T>(x, acc);
+}
+template <int L, int P>
+__device__ __forceinline__ void joint_pow2_step(const uint32_t* w, uint32_t lane4) {
+  uint32_t a = joint_field<L, 3 * P + 2, 7>(w, lane4);      // B: bits 7 ..
+  a = joint_field<L, 3 * P + 1, L + 7>(w, a);               // G
+  red_shared_add_off<0>(joint_field<L, 3 * P, 2 * L + 7>(w, a));  // R
+}
+template <int L, int... P>
+__device__ __forceinline__ void joint_pow2_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
+  (joint_pow2_step<L, P>(w, lane4), ...);
+}
+template <int L>
+__device__ __forceinline__ void hist_unit_joint_pow2(const uint32_t* w, uint32_t lane4) {
+  joint_pow2_all<L>(w, lane4, std::make_integer_sequence<int, 16>{});
+}
+
 __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {  // 48 bytes at a 16-byte aligned address
   const uint4 v0 = lds128(a), v1 = lds128(a + 16), v2 = lds128(a + 32);
   w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
@@ -407,6 +453,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);  // 3 x 16 bins (pair modes)
   uint32_t* remap = reinterpret_cast<uint32_t*>(smem + (L.table + p.table_bytes - base));  // kRaw: 3 x B bins
   const int B = p.bins;
+  const int RS = MODE == kModeJoint ? p.joint * p.joint * p.joint : 3 * B;  // counters per output row
 
   if (threadIdx.x == 0) {
     if (L.stages < 2) __trap();
@@ -487,7 +534,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   int64_t cur = -1;
 
   auto out_row = [&](int64_t item) -> uint32_t* {
-    return item < p.n_halo ? p.halo_out + item * 3 * B : p.out + (item - p.n_halo) * 3 * B;
+    return item < p.n_halo ? p.halo_out + item * RS : p.out + (item - p.n_halo) * RS;
   };
   // add v to counter idx of item's row: locally, or (fused all-gather) into the same row of
   // every rank's result column through peer memory (NVLink when the dest is on another GPU)
@@ -495,7 +542,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     if (p.n_dest == 0 || item < p.n_halo) {
       red_global_add(out_row(item) + idx, v);
     } else {
-      const int64_t off = (item - p.n_halo) * 3 * B + idx;
+      const int64_t off = (item - p.n_halo) * RS + idx;
       for (int g = 0; g < p.n_dest; ++g) red_global_add(reinterpret_cast<uint32_t*>(p.dest[g]) + off, v);
     }
   };
@@ -538,8 +585,21 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     } else {
 #pragma unroll
       for (int i = 0; i < kSnapN; ++i) {
-        const int r = ctid + i * kConsThreads;  // row (c, key) = (r >> 8, r & 255)
-        if (r >= 768) break;
+        const int r = ctid + i * kConsThreads;  // row (c, key) = (r >> 8, r & 255); kModeJoint: the joint bin
+        if (r >= (MODE == kModeJoint ? RS : 768)) break;
+        if constexpr (MODE == kModeJoint) {
+          uint32_t sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 v = lds128(L.table + (uint32_t)r * 128u + (uint32_t)(((j + r) & 7) * 16));
+            sum += v.x + v.y + v.z + v.w;
+          }
+          const uint32_t total = sum;
+          sum = total - snap[i];
+          snap[i] = total;
+          if (sum) emit(item, r, sum);
+          continue;
+        }
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         uint32_t sum = 0;
         if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
@@ -581,7 +641,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           if (v) emit(item, i, v);
         }
       }
-    } else if (ctid < 3 * B) {  // B divides 16: bin b of channel c merges 16/B adjacent 16-level bins
+    } else if (MODE != kModeJoint && ctid < 3 * B) {  // B divides 16: bin b of channel c merges 16/B adjacent 16-level bins
       const int c = ctid / B, b = ctid - c * B, g = 16 / B;
       uint32_t v = 0;
       for (int k = 0; k < g; ++k) {
@@ -740,6 +800,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           hist_unit_pair<false>(w, lane4);
         } else if constexpr (MODE == kModeRaw) {
           hist_unit_raw(w, lane4);
+        } else if constexpr (MODE == kModeJoint) {
+          switch (p.joint) {  // uniform over the launch
+            case 1: hist_unit_joint_pow2<0>(w, lane4); break;
+            case 2: hist_unit_joint_pow2<1>(w, lane4); break;
+            case 4: hist_unit_joint_pow2<2>(w, lane4); break;
+            case 8: hist_unit_joint_pow2<3>(w, lane4); break;
+            default: hist_unit_joint(w, lane4, (uint32_t)p.joint);
+          }
         } else if constexpr (MODE == kModeMatch) {
           // north_star K2a: per-warp bins, peers found with __match_any_sync, one leader
           // atomic of popc(peers) per peer group
@@ -763,7 +831,13 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       }
       // tail bytes (frame size not a multiple of 48): direct global counts of the true bin
       const uint32_t rem = len - nunits * 48u;
-      if ((uint32_t)ctid < rem) {
+      if constexpr (MODE == kModeJoint) {  // whole pixels (tiles and frames are multiples of 3 bytes)
+        if ((uint32_t)ctid < rem / 3u) {
+          const uint32_t a = slot + nunits * 48u + 3u * (uint32_t)ctid, J = (uint32_t)p.joint;
+          const uint32_t k = (((lds_u8(a) * J) >> 8) * J + ((lds_u8(a + 1) * J) >> 8)) * J + ((lds_u8(a + 2) * J) >> 8);
+          emit(item, (int)k, 1u);
+        }
+      } else if ((uint32_t)ctid < rem) {
         const uint32_t j = nunits * 48u + (uint32_t)ctid;
         const uint32_t v = lds_u8(slot + j);
         emit(item, (int)((j % 3) * B + ((v * (uint32_t)B) >> 8)), 1u);
@@ -1032,6 +1106,7 @@ static HistParams base_params(const HistJob& j) {
   p.width = j.width;
   p.height = j.height;
   p.bins = j.bins;
+  p.joint = j.joint;
   p.smem_bytes = (uint32_t)g_smem_optin;
   p.max_stages = knobs().max_stages;
   p.prod_sleep = knobs().prod_sleep;
@@ -1079,6 +1154,25 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
   if (knobs().hist_warps == 20) return launch_tma<kModeRaw, 20>(p, st);
 #endif
   return launch_tma<kModeRaw, kHistWarps>(p, st);
+}
+
+// NEXT N4 joint-colour histogram: J bins per channel (1..8), J^3 lane-private rows.
+cudaError_t launch_histogram_joint(const HistJob& j, cudaStream_t st, int* launches) {
+  cudaError_t e = device_props();
+  if (e != cudaSuccess) return e;
+  if (j.n_items <= 0) return cudaSuccess;
+  HistParams p = base_params(j);
+  p.ds_out = nullptr;
+  p.tile = p.slot = kTile;
+  p.rows_per_tile = 0;
+  p.tpf = (int32_t)((p.F + p.tile - 1) / p.tile);
+  p.total_tiles = p.n_items * p.tpf;
+  p.l2_prefetch = knobs().l2_prefetch_hist;
+  p.table_bytes = (uint32_t)(j.joint * j.joint * j.joint) * 128u;
+  // J = 2^L ORs the bin fields into the table address: align the table to its own size
+  p.table_align = (j.joint & (j.joint - 1)) == 0 ? p.table_bytes : 128u;
+  *launches += 1;
+  return launch_tma<kModeJoint, kHistWarps>(p, st);
 }
 
 // Row-pair tiling of frames for the fused / downsample-only kernels.

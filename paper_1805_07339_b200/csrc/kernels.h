@@ -21,6 +21,7 @@ struct HistJob {
   uint32_t* halo_out;  // [n_halo][3][bins]
   uint8_t* ds_out;     // fused downsample output [n_items - n_halo][H/2][W/2][3] or nullptr
   int32_t width, height, bins;
+  int32_t joint;       // launch_histogram_joint: J bins per channel (rows of J^3 counters)
   int64_t ds_pitch;    // bytes between output rows (0: (W/2)*3, contiguous frames)
   int32_t ds_cols;     // > 0: montage, frame i is tile (i / cols, i % cols) of a canvas (NEXT N1)
   int32_t n_dest;      // > 0: non-halo rows go to every dest[g] (row 0 = item n_halo) instead of out
@@ -37,6 +38,8 @@ cudaError_t launch_zero_dests(const DestList& d, int64_t words, cudaStream_t st,
 // Histogram (zeroes nothing: the caller memsets out/halo_out first).
 // Returns the number of kernel launches in *launches.
 cudaError_t launch_histogram(const HistJob& job, cudaStream_t st, int* launches);
+// NEXT N4 joint-colour histogram (job.joint = J in [1, 8]; out rows of J^3 counters, zeroed by the caller).
+cudaError_t launch_histogram_joint(const HistJob& job, cudaStream_t st, int* launches);
 // Fused HIST + downsample; falls back to two passes for shapes the fused kernel does not take.
 cudaError_t launch_hist_downsample(const HistJob& job, cudaStream_t st, int* launches);
 // Shot-diff over n positions, D[p] written to every d.p[g] + p (d.n = 1 for a plain run);

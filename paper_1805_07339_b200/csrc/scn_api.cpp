@@ -514,6 +514,34 @@ scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32
   return run_hist(s, begin, end - begin, 0, bins, d_hist, nullptr, nullptr, (cudaStream_t)stream);
 }
 
+scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
+                                   uint32_t* d_hist, void* stream) {
+  scn_status rc = check_run(s, begin, end, 0, false);
+  if (rc) return rc;
+  if (bins_per_channel < 1 || bins_per_channel > 8)
+    return fail(SCN_EUNSUPPORTED, "joint bins per channel must be in [1,8], got %d", bins_per_channel);
+  if (end == begin) return SCN_OK;
+  if (!d_hist) return fail(SCN_EINVAL, "d_hist is NULL");
+  if ((rc = check_resident(s, begin, end))) return rc;
+  const int64_t n = end - begin, K = (int64_t)bins_per_channel * bins_per_channel * bins_per_channel;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(d_hist, 0, (size_t)(n * K) * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(joint hist)");
+  scn::HistJob j{};
+  j.src.ptrs = d_addr(s) + begin;
+  j.n_items = n;
+  j.out = d_hist;
+  j.width = s->width;
+  j.height = s->height;
+  j.bins = bins_per_channel;
+  j.joint = bins_per_channel;
+  int nl = 0;
+  e = scn::launch_histogram_joint(j, st, &nl);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "joint histogram launch");
+  return SCN_OK;
+}
+
 static scn_status run_diff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, const uint32_t* d_hist,
                            const uint32_t* halo, uint32_t* d_diff, cudaStream_t st) {
   int nl = 0;

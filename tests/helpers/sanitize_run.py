@@ -64,8 +64,22 @@ def main():
         scn.scn_set_hist_impl(impl)
         check(w1, ("hist", "shotdiff"), 16)
     scn.scn_set_hist_impl(0)
+    joint(w2, 4)
+    joint(w1, 3)
     next_rows()
     print("sanitize_run ok")
+
+
+def joint(wl, j):
+    import paper_1805_07339_b200 as scn
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    job = scn_harness.DeviceJob(wl, 0, M, with_halo=False, plan_=pl)
+    out = torch.empty((M, j ** 3), dtype=torch.int32, device="cuda")
+    scn.scn_run_histogram_joint(job.seq, 0, M, j, out, job.stream)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint32) == oracle.run_joint(wl.spec(), pl[0], pl[1], 0, M, j)).all()
+    job.close()
 
 
 def unaligned_out(wl):
