@@ -37,6 +37,9 @@ run ds_1366 2048 C4 ds 0 1366x768 0
 run histds_854 4096 C4 histds 0 854x480 0
 run hist_k2a 128 C2 hist 0 "" 1
 run hist_k2ap 512 C2 hist 0 "" 2
+REPS=1 timeout 900 ncu --metrics $M --clock-control none -k regex:hist_tma_kernel -s 3 -c 1 --csv \
+  --log-file $O/counters_hist_joint8.csv python bench.py --joint 8 --frames 2048 --steps 1 --warmup 3 > $O/counters_hist_joint8.log 2>&1
+python tools/ncu_summarize.py $O/counters_hist_joint8.csv hist_joint8 2048 C2 hist 0 "" $SHA > $O/counters_hist_joint8.json
 # full-set captures of the two headline kernels -> traffic summaries (bytes per frame, SHA)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:hist_tma_kernel -s 3 -c 1 -o $O/full_hist \
   python tools/hist_tune.py shots 2048 C2 hist --reps 1 > $O/full_hist.log 2>&1; echo "full hist $?"

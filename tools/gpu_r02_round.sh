@@ -28,6 +28,7 @@ $B --montage 8 --steps 10 > $O/bench_C2_montage8.json 2>/dev/null; echo "montage
 for m in uniform constant xgrad; do $B --mode $m --no-cpu-baseline --no-e2e > $O/bench_C2_$m.json 2>/dev/null; echo "$m $?"; done
 for impl in 1 2; do $B --hist-impl $impl --frames 1024 --steps 5 --no-cpu-baseline --no-e2e > $O/bench_C2_k2a_impl$impl.json 2>/dev/null; echo "k2a $impl $?"; done
 for g in nccl p2p; do timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr=127.0.0.1 --master-port=$((20000 + RANDOM % 20000)) bench.py --gpus 2 --dist-backend gloo --gather $g --no-e2e --no-cpu-baseline --steps 10 > $O/bench_n2_shared_gpu_$g.json 2>$O/bench_n2_shared_gpu_$g.err; echo "n2 $g $?"; done
+for j in 8 4 3; do $B --joint $j > $O/bench_C2_joint$j.json 2>/dev/null; echo "joint $j $?"; done
 $B --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2>/dev/null; echo "ref $?"
 NCU_OUT=$O/ncu bash tools/gpu_r02_ncu.sh > $O/ncu_pass.log 2>&1; echo "ncu $?"
 T="python tools/hist_tune.py shots"
