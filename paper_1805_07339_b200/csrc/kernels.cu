@@ -38,6 +38,9 @@
 //   merge across warps, one global add per key per block.
 // K2a'   MODE kMatchPacked  K2a amortised: one __match_any_sync per packed word of four
 //   pair keys (8 bytes), so MATCH issues 1/8 as often; per-warp pair-key bins.
+// K2j    MODE kJoint (NEXT N4's joint-colour variant): one key per pixel,
+//   k = bin(R)*J*J + bin(G)*J + bin(B), J <= 8, into J^3 lane-private 128-byte rows; for J = 2^L
+//   each channel's bin field is cut with one SHF and OR-ed into the row address with one LOP3.
 // K3     shotdiff_kernel: one warp per position, L1 over 3*B counters, __reduce_add_sync.
 //
 // Why not the north_star's per-warp bins + __match_any_sync aggregation as the default:
