@@ -784,13 +784,14 @@ def run_b200(args):
             line["config"]["gather_note"] = gather_note
         if graph_note:
             line["config"]["graph_note"] = graph_note
-        print(json.dumps(line), flush=True)
     graphs.clear()
     job.close()
     if peer is not None:
         peer.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:  # last, after teardown: NCCL's INIT log (stdout) cannot follow the JSON line
+        print(json.dumps(line), flush=True)
     return 0
 
 
