@@ -48,6 +48,8 @@ def lib():
                                         ctypes.c_void_p]
         L.oracle_run_joint.argtypes = [ctypes.POINTER(scn_synth.SynthSpecC), ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+        L.oracle_shotdiff_joint.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                            ctypes.c_void_p]
         L.oracle_shotdiff.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.c_void_p]
         L.oracle_downsample.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
@@ -143,6 +145,34 @@ def run_joint(spec: "scn_synth.Spec", videos, rows, p0: int, p1: int, j: int = 4
     if rc:
         raise OracleError(rc, "run_joint")
     return out[:n]
+
+
+def shotdiff_joint(hists: np.ndarray, seg_start=None) -> np.ndarray:
+    """[-1,0] L1 difference of joint-colour histograms [M, J^3] -> uint32 [M] (0 at segment starts)."""
+    hh = np.ascontiguousarray(hists, dtype=np.uint32)
+    m, k = hh.shape
+    j = round(k ** (1 / 3))
+    assert j ** 3 == k
+    seg = np.zeros(max(m, 1), dtype=np.uint8)
+    if seg_start is not None:
+        seg[:m] = np.asarray(seg_start, dtype=np.uint8)
+    if m:
+        seg[0] = 1
+    out = np.zeros(max(m, 1), dtype=np.uint32)
+    rc = lib().oracle_shotdiff_joint(_ptr(hh), _ptr(seg), m, j, _ptr(out))
+    if rc:
+        raise OracleError(rc, "shotdiff_joint")
+    return out[:m]
+
+
+def run_joint_diff(spec: "scn_synth.Spec", videos, rows, seg_start, p0: int, p1: int, j: int = 4):
+    """Joint-colour histograms and their [-1,0] shot-diff for positions [p0, p1); position p0's
+    stencil neighbour p0-1 (the halo) is included when p0 is not a segment start."""
+    seg = np.asarray(seg_start, dtype=np.uint8)
+    lo = p0 - 1 if (0 < p0 < len(seg) and not seg[p0]) else p0
+    H = run_joint(spec, videos, rows, lo, p1, j)
+    D = shotdiff_joint(H, seg[lo:p1])
+    return H[p0 - lo:], D[p0 - lo:]
 
 
 def shotdiff(hists: np.ndarray, seg_start=None) -> np.ndarray:

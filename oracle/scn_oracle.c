@@ -192,6 +192,25 @@ int oracle_shotdiff(const uint32_t* hist, const uint8_t* seg_start, int64_t m, i
   return OR_OK;
 }
 
+/* Shot-diff over joint-colour histograms (NEXT N4's joint variant with the same
+ * [-1,0] L1 stencil of P:L455 / P:L210, readings Q4, Q6, Q7): diff[p] =
+ * sum_k |hist[p][k] - hist[p-1][k]| over the J^3 counters, 0 at segment starts.
+ * hist: [m][J^3]. */
+int oracle_shotdiff_joint(const uint32_t* hist, const uint8_t* seg_start, int64_t m, int32_t j, uint32_t* diff) {
+  if (j < 1 || j > 16) return OR_EUNSUPPORTED;
+  const int64_t k = (int64_t)j * j * j;
+  for (int64_t p = 0; p < m; ++p) {
+    int64_t q = (p == 0 || seg_start[p]) ? p : p - 1; /* clamp the -1 offset */
+    uint32_t d = 0;
+    for (int64_t i = 0; i < k; ++i) {
+      uint32_t a = hist[p * k + i], b = hist[q * k + i];
+      d += a > b ? a - b : b - a;
+    }
+    diff[p] = d;
+  }
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------------------
  * Downsample: integer 2x box ("downsamples the resulting frames
  * (Resize)", "Downsample and transform an input frame"). Reading Q11:

@@ -72,3 +72,50 @@ def test_rejects_bad_bins():
     for j in (0, 17):
         with pytest.raises(oracle.OracleError):
             oracle.hist_joint(f, j)
+
+
+def _const(rgb, w=5, h=4):
+    f = np.empty((h, w, 3), np.uint8)
+    f[:] = rgb
+    return f
+
+
+@pytest.mark.parametrize("j", [2, 3, 4, 8])
+def test_joint_shotdiff_closed_forms(j):
+    # identical frames -> 0; constant frames A -> B -> 2*W*H if their joint bins differ, else 0
+    A, B, C = (10, 200, 30), (250, 40, 128), (12, 201, 31)
+    hs = np.stack([oracle.hist_joint(_const(x), j) for x in (A, A, B, C, C)])
+    d = oracle.shotdiff_joint(hs)
+    kk = lambda x: ((x[0] * j // 256) * j + x[1] * j // 256) * j + x[2] * j // 256  # noqa: E731
+    expect = [0, 0, 2 * 20 * (kk(A) != kk(B)), 2 * 20 * (kk(B) != kk(C)), 0]
+    np.testing.assert_array_equal(d, expect)
+    # segment starts clamp to 0
+    np.testing.assert_array_equal(oracle.shotdiff_joint(hs, [1, 0, 1, 0, 0]), [0, 0, 0, expect[3], 0])
+
+
+def test_joint_shotdiff_planted_cuts_c1():
+    # C1's three planted cuts move every channel's base colour >= 65 levels, so at J = 4 (64-level
+    # bins) nearly every pixel changes joint bin there (D close to its 2*W*H maximum); inside
+    # shots D stays far below W*H
+    wl = scn_synth.WORKLOADS["C1"]
+    import scn_harness
+    part, row, seg = scn_harness.plan(wl)
+    H, D = oracle.run_joint_diff(wl.spec(), part, row, seg, 0, len(row), 4)
+    wh = wl.width * wl.height
+    assert set(np.nonzero(D > wh)[0].tolist()) == {57, 131, 198}
+    assert (D[[57, 131, 198]] > 1.9 * wh).all() and (D <= 2 * wh).all()
+    # the halo: a shard starting inside the film reproduces the full run's values
+    H2, D2 = oracle.run_joint_diff(wl.spec(), part, row, seg, 100, len(row), 4)
+    np.testing.assert_array_equal(D2, D[100:])
+    np.testing.assert_array_equal(H2, H[100:])
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_joint_shotdiff_metric_properties(seed):
+    rng = np.random.default_rng(seed)
+    fr = [rng.integers(0, 256, size=(6, 7, 3), dtype=np.uint8) for _ in range(3)]
+    h = [oracle.hist_joint(f, 4).astype(np.int64) for f in fr]
+    l1 = lambda a, b: int(oracle.shotdiff_joint(np.stack([a, b]))[1])  # noqa: E731
+    assert l1(h[0], h[1]) == l1(h[1], h[0]) == int(np.abs(h[0] - h[1]).sum())
+    assert l1(h[0], h[2]) <= l1(h[0], h[1]) + l1(h[1], h[2])
+    assert l1(h[0], h[1]) <= 2 * 6 * 7 and l1(h[0], h[1]) % 2 == 0
