@@ -360,8 +360,9 @@ def run_montage(args):
 
 
 def run_joint(args):
-    """NEXT N4, joint-colour variant: scn_run_histogram_joint (J bins per channel, J^3 counters
-    per frame) over the config's sampled frames, device-resident, N = 1."""
+    """NEXT N4, joint-colour variant: scn_run_hist_shotdiff_joint (J bins per channel, J^3 counters
+    per frame, then the [-1,0] L1 shot-diff over them) over the config's sampled frames,
+    device-resident, N = 1."""
     import torch
 
     import paper_1805_07339_b200 as scn
@@ -379,9 +380,11 @@ def run_joint(args):
                                 spec=wl.spec(mode=args.mode))
     J = args.joint
     out = torch.empty((max(M, 1), J ** 3), dtype=torch.int32, device=dev)
+    diff = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+    scratch = torch.empty(J ** 3, dtype=torch.int32, device=dev)
 
     def step():
-        scn.scn_run_histogram_joint(job.seq, 0, M, J, out, st)
+        scn.scn_run_hist_shotdiff_joint(job.seq, 0, M, J, out, diff, scratch, st)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -402,17 +405,18 @@ def run_joint(args):
     ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     step_ms = float(np.mean(ms))
     peak, peak_src = load_peaks()
-    alg = M * (wl.frame_bytes + J ** 3 * 4)
+    # histogram: frame read + row write; shot-diff: two row reads + D write (SURVEY §8(d) per frame)
+    alg = M * (wl.frame_bytes + J ** 3 * 4 * 3 + 4)
     ach = alg / (step_ms / 1e3) / 1e9
     line = {"metric": METRIC, "value": M / (step_ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl.name + f" joint-colour histogram J={J} (NEXT N4)", "frames": M,
                        "width": wl.width, "height": wl.height, "joint_bins": J ** 3, "content": args.mode,
-                       "ops": "hist_joint", "l2": "no flush: input %.1f GB >> 126 MB L2" % (M * wl.frame_bytes / 1e9)},
+                       "ops": "hist_joint+shotdiff_joint", "l2": "no flush: input %.1f GB >> 126 MB L2" % (M * wl.frame_bytes / 1e9)},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
-                         "kernel": "hist_tma_kernel<7,16> (scn_run_histogram_joint incl. memset)",
+                         "kernel": "hist_tma_kernel<7,16> + shotdiff_kernel (whole step incl. memset)",
                          **stream_ceiling(False, ach)},
             "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps, "clocks": clk,
             "step_ms_min": float(min(ms)), "library": scn.scn_version()}

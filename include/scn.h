@@ -157,6 +157,18 @@ scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32
 scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
                                    uint32_t* d_hist, void* stream);
 
+/* Shot-diff over joint-colour histograms (NEXT N4 joint variant with the same
+ * [-1,0] L1 stencil as scn_run_shotdiff, P:L455 / P:L210, readings Q6, Q7):
+ * d_hist as scn_run_histogram_joint ([end-begin][J^3] u32, zeroed by the call);
+ * d_diff[j] (u32) = sum_k |H[j][k] - H[j-1][k]| over the J^3 counters, 0 at
+ * the first position of a part. If scn_seq_needs_halo(s, begin), the joint
+ * histogram of position begin-1 rides in the same launch into d_scratch
+ * (>= J^3 u32; recomputed, not communicated). EUNSUPPORTED if J is
+ * outside [1,8]; EINVAL on NULL d_hist / d_diff (or d_scratch when a halo is
+ * needed); ERANGE if a read position is not resident. */
+scn_status scn_run_hist_shotdiff_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
+                                       uint32_t* d_hist, uint32_t* d_diff, uint32_t* d_scratch, void* stream);
+
 /* Shot-diff ("detect shot boundaries (via histogram differences)") as
  * a [-1,0] stencil over the sampled sequence (fig:sampling-f; reading
  * Q7): d_diff[j] (u32) = sum_c sum_b |H[j][c][b] - H[j-1][c][b]|, and 0 at the

@@ -69,6 +69,7 @@ _sig("scn_seq_upload", ctypes.c_int, _vp, _vp, _sz, _vp)
 _sig("scn_seq_destroy", None, _vp)
 _sig("scn_run_histogram", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp)
 _sig("scn_run_histogram_joint", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp)
+_sig("scn_run_hist_shotdiff_joint", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_hist_shotdiff", ctypes.c_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp)
 _sig("scn_run_downsample", ctypes.c_int, _vp, _i64, _i64, _vp, _vp)
@@ -236,6 +237,11 @@ def scn_run_histogram(s, begin, end, bins, d_hist, stream=None) -> None:
 def scn_run_histogram_joint(s, begin, end, bins_per_channel, d_hist, stream=None) -> None:
     _check(_lib.scn_run_histogram_joint(s, begin, end, bins_per_channel, _ptr(d_hist), _stream(stream)),
            "scn_run_histogram_joint")
+
+
+def scn_run_hist_shotdiff_joint(s, begin, end, bins_per_channel, d_hist, d_diff, d_scratch=None, stream=None) -> None:
+    _check(_lib.scn_run_hist_shotdiff_joint(s, begin, end, bins_per_channel, _ptr(d_hist), _ptr(d_diff),
+                                            _ptr(d_scratch), _stream(stream)), "scn_run_hist_shotdiff_joint")
 
 
 def scn_run_shotdiff(s, begin, end, bins, d_hist, d_diff, d_scratch=None, stream=None) -> None:

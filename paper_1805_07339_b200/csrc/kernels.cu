@@ -855,17 +855,17 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
 }
 
 // ---------------------------------------------------------------------------
-// K3: shot-diff. One warp per position; D goes to every destination column
-// (d.n == 1 and d.p[0] = the caller's column for a plain run).
+// K3: shot-diff. One warp per position, L1 over the K counters of a row (3*B per-channel,
+// J^3 joint-colour); D goes to every destination column (d.n == 1 and d.p[0] = the
+// caller's column for a plain run).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) shotdiff_kernel(const uint32_t* __restrict__ hist,
                                                         const uint32_t* __restrict__ halo,
-                                                        const uint8_t* __restrict__ seg, int64_t n, int32_t bins,
+                                                        const uint8_t* __restrict__ seg, int64_t n, int32_t K,
                                                         DestList d) {
   const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (pos >= n) return;
-  const int K = 3 * bins;
   uint32_t s = 0;
   if (!seg[pos]) {
     const uint32_t* cur = hist + pos * K;
@@ -1251,10 +1251,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
 }
 
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
-                            int32_t bins, const DestList& d, cudaStream_t st, int* launches) {
+                            int32_t row, const DestList& d, cudaStream_t st, int* launches) {
   if (n <= 0) return cudaSuccess;
   *launches += 1;
-  shotdiff_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(hist, halo_row, seg, n, bins, d);
+  shotdiff_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(hist, halo_row, seg, n, row, d);
   return cudaGetLastError();
 }
 

@@ -42,11 +42,11 @@ cudaError_t launch_histogram(const HistJob& job, cudaStream_t st, int* launches)
 cudaError_t launch_histogram_joint(const HistJob& job, cudaStream_t st, int* launches);
 // Fused HIST + downsample; falls back to two passes for shapes the fused kernel does not take.
 cudaError_t launch_hist_downsample(const HistJob& job, cudaStream_t st, int* launches);
-// Shot-diff over n positions, D[p] written to every d.p[g] + p (d.n = 1 for a plain run);
+// Shot-diff over n positions of `row` u32 counters each (3*B, or J^3 joint), D[p] written to every d.p[g] + p (d.n = 1 for a plain run);
 // seg[p] != 0 marks a segment start; halo_row is the histogram of the position before the
 // first (used iff !seg[0]).
 cudaError_t launch_shotdiff(const uint32_t* hist, const uint32_t* halo_row, const uint8_t* seg, int64_t n,
-                            int32_t bins, const DestList& d, cudaStream_t st, int* launches);
+                            int32_t row, const DestList& d, cudaStream_t st, int* launches);
 // D[j] = sum |H[a[j]] - H[b[j]]| (NEXT N2: stencil before sampling)
 cudaError_t launch_diff_pairs(const uint32_t* hist, const int64_t* a, const int64_t* b, int64_t n, int32_t bins,
                               uint32_t* diff, cudaStream_t st, int* launches);

@@ -514,27 +514,24 @@ scn_status scn_run_histogram(const scn_seq* s, int64_t begin, int64_t end, int32
   return run_hist(s, begin, end - begin, 0, bins, d_hist, nullptr, nullptr, (cudaStream_t)stream);
 }
 
-scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
-                                   uint32_t* d_hist, void* stream) {
-  scn_status rc = check_run(s, begin, end, 0, false);
-  if (rc) return rc;
-  if (bins_per_channel < 1 || bins_per_channel > 8)
-    return fail(SCN_EUNSUPPORTED, "joint bins per channel must be in [1,8], got %d", bins_per_channel);
-  if (end == begin) return SCN_OK;
-  if (!d_hist) return fail(SCN_EINVAL, "d_hist is NULL");
-  if ((rc = check_resident(s, begin, end))) return rc;
-  const int64_t n = end - begin, K = (int64_t)bins_per_channel * bins_per_channel * bins_per_channel;
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(d_hist, 0, (size_t)(n * K) * sizeof(uint32_t), st);
+// joint-colour histograms of n_items positions from `first`; the first n_halo go to d_halo
+static scn_status run_hist_joint(const scn_seq* s, int64_t first, int64_t n_items, int32_t n_halo, int32_t J,
+                                 uint32_t* d_hist, uint32_t* d_halo, cudaStream_t st) {
+  const size_t row = (size_t)J * J * J * sizeof(uint32_t);
+  cudaError_t e = cudaSuccess;
+  if (n_items - n_halo > 0) e = cudaMemsetAsync(d_hist, 0, row * (size_t)(n_items - n_halo), st);
+  if (e == cudaSuccess && n_halo) e = cudaMemsetAsync(d_halo, 0, row * (size_t)n_halo, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(joint hist)");
   scn::HistJob j{};
-  j.src.ptrs = d_addr(s) + begin;
-  j.n_items = n;
+  j.src.ptrs = d_addr(s) + first;
+  j.n_items = n_items;
+  j.n_halo = n_halo;
   j.out = d_hist;
+  j.halo_out = d_halo;
   j.width = s->width;
   j.height = s->height;
-  j.bins = bins_per_channel;
-  j.joint = bins_per_channel;
+  j.bins = J;
+  j.joint = J;
   int nl = 0;
   e = scn::launch_histogram_joint(j, st, &nl);
   g_launches += nl;
@@ -542,10 +539,47 @@ scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end,
   return SCN_OK;
 }
 
+static scn_status check_joint(int32_t J) {
+  if (J < 1 || J > 8) return fail(SCN_EUNSUPPORTED, "joint bins per channel must be in [1,8], got %d", J);
+  return SCN_OK;
+}
+
+scn_status scn_run_histogram_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
+                                   uint32_t* d_hist, void* stream) {
+  scn_status rc = check_run(s, begin, end, 0, false);
+  if (rc || (rc = check_joint(bins_per_channel))) return rc;
+  if (end == begin) return SCN_OK;
+  if (!d_hist) return fail(SCN_EINVAL, "d_hist is NULL");
+  if ((rc = check_resident(s, begin, end))) return rc;
+  return run_hist_joint(s, begin, end - begin, 0, bins_per_channel, d_hist, nullptr, (cudaStream_t)stream);
+}
+
+scn_status scn_run_hist_shotdiff_joint(const scn_seq* s, int64_t begin, int64_t end, int32_t bins_per_channel,
+                                       uint32_t* d_hist, uint32_t* d_diff, uint32_t* d_scratch, void* stream) {
+  scn_status rc = check_run(s, begin, end, 0, false);
+  if (rc || (rc = check_joint(bins_per_channel))) return rc;
+  if (end == begin) return SCN_OK;
+  if (!d_hist || !d_diff) return fail(SCN_EINVAL, "d_hist/d_diff is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int32_t halo = scn_seq_needs_halo(s, begin);
+  if (halo && !d_scratch) return fail(SCN_EINVAL, "d_scratch needed for the halo histogram");
+  if ((rc = check_resident(s, begin - halo, end))) return rc;
+  const int32_t J = bins_per_channel;
+  // the halo frame (position begin-1) is recomputed in the same launch
+  rc = run_hist_joint(s, begin - halo, end - begin + halo, halo, J, d_hist, d_scratch, st);
+  if (rc) return rc;
+  int nl = 0;
+  cudaError_t e = scn::launch_shotdiff(d_hist, halo ? d_scratch : nullptr, d_seg(s) + begin, end - begin,
+                                       J * J * J, one_dest(d_diff), st, &nl);
+  g_launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "joint shotdiff launch");
+  return SCN_OK;
+}
+
 static scn_status run_diff(const scn_seq* s, int64_t begin, int64_t end, int32_t bins, const uint32_t* d_hist,
                            const uint32_t* halo, uint32_t* d_diff, cudaStream_t st) {
   int nl = 0;
-  cudaError_t e = scn::launch_shotdiff(d_hist, halo, d_seg(s) + begin, end - begin, bins, one_dest(d_diff), st, &nl);
+  cudaError_t e = scn::launch_shotdiff(d_hist, halo, d_seg(s) + begin, end - begin, 3 * bins, one_dest(d_diff), st, &nl);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "shotdiff launch");
   return SCN_OK;
@@ -630,7 +664,7 @@ scn_status scn_run_hist_shotdiff_to(const scn_seq* s, int64_t begin, int64_t end
   e = scn::launch_histogram(j, st, &nl);
   if (e == cudaSuccess)
     e = scn::launch_shotdiff(reinterpret_cast<const uint32_t*>(dh.p[self]), halo ? d_scratch : nullptr,
-                             d_seg(s) + begin, n, bins, dd, st, &nl);
+                             d_seg(s) + begin, n, (int32_t)K, dd, st, &nl);
   g_launches += nl;
   if (e != cudaSuccess) return cuda_fail(e, "hist_shotdiff_to launch");
   return SCN_OK;
@@ -815,7 +849,7 @@ scn_status scn_run_pipeline_host(const scn_seq* s, int64_t begin, int64_t end, i
   }
   if (e == cudaSuccess && do_diff) {
     int nl = 0;
-    e = scn::launch_shotdiff(d_hist, halo ? d_scratch : nullptr, (const uint8_t*)d_staging, n, bins,
+    e = scn::launch_shotdiff(d_hist, halo ? d_scratch : nullptr, (const uint8_t*)d_staging, n, 3 * bins,
                              one_dest(d_diff), st, &nl);
     g_launches += nl;
   }

@@ -65,3 +65,90 @@ def test_unsupported_bins():
             scn.scn_run_histogram_joint(job.seq, 0, 2, j, out)
         assert e.value.status == scn.SCN_EUNSUPPORTED
     job.close()
+
+
+# --- shot-diff over joint-colour histograms (scn_run_hist_shotdiff_joint) ---------------------
+
+def _joint_diff(wl, j, p0, p1, mode="shots", pl=None):
+    pl = pl if pl is not None else scn_harness.plan(wl)
+    spec = wl.spec(mode=mode)
+    job = scn_harness.DeviceJob(wl, p0, p1, with_halo=True, spec=spec, plan_=pl)
+    n = p1 - p0
+    H = torch.full((max(n, 1), j ** 3), -1, dtype=torch.int32, device="cuda")
+    D = torch.full((max(n, 1),), -1, dtype=torch.int32, device="cuda")
+    scratch = torch.full((j ** 3,), -1, dtype=torch.int32, device="cuda")
+    scn.scn_run_hist_shotdiff_joint(job.seq, p0, p1, j, H, D, scratch, job.stream)
+    nl = scn.scn_last_launch_count()
+    torch.cuda.synchronize()
+    got_h = H.cpu().numpy().view(np.uint32)[:n]
+    got_d = D.cpu().numpy().view(np.uint32)[:n]
+    job.close()
+    ref_h, ref_d = oracle.run_joint_diff(spec, pl[0], pl[1], pl[2], p0, p1, j)
+    return got_h, got_d, ref_h, ref_d, nl
+
+
+@pytest.mark.parametrize("j", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("w,h", [(1, 1), (17, 9), (67, 41), (640, 49)])
+def test_joint_shotdiff_shapes(j, w, h):
+    wl = Workload("jdiff", w, h, 3, 11, ("stride", 1), ("hist", "shotdiff"), spec_kw={"len_min": 2, "len_max": 4})
+    M = len(scn_harness.plan(wl)[1])
+    gh, gd, rh, rd, nl = _joint_diff(wl, j, 0, M)
+    np.testing.assert_array_equal(gh, rh)
+    np.testing.assert_array_equal(gd, rd)
+    assert nl == 2  # one histogram launch (memset is not a kernel of ours) + one shot-diff launch
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("j", [3, 4, 8])
+def test_joint_shotdiff_virtual_shards(world, j):
+    # every shard recomputes its [-1,0] halo; the concatenation equals the single run and the oracle
+    wl = Workload("jshard", 96, 54, 2, 13, ("stride", 2), ("hist", "shotdiff"), spec_kw={"len_min": 2, "len_max": 5})
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    hs, ds = [], []
+    for r in range(world):
+        b, e = scn.scn_shard_range(M, world, r)
+        gh, gd, rh, rd, _ = _joint_diff(wl, j, b, e, pl=pl)
+        np.testing.assert_array_equal(gh, rh)
+        np.testing.assert_array_equal(gd, rd)
+        hs.append(gh)
+        ds.append(gd)
+    full_h, full_d, _, _, _ = _joint_diff(wl, j, 0, M, pl=pl)
+    np.testing.assert_array_equal(np.concatenate(hs), full_h)
+    np.testing.assert_array_equal(np.concatenate(ds), full_d)
+
+
+def test_joint_shotdiff_c1_planted_cuts():
+    wl = scn_synth.WORKLOADS["C1"]
+    pl = scn_harness.plan(wl)
+    M = len(pl[1])
+    gh, gd, rh, rd, _ = _joint_diff(wl, 4, 0, M, pl=pl)
+    np.testing.assert_array_equal(gd, rd)
+    np.testing.assert_array_equal(gh, rh)
+    # the planted cuts move nearly every pixel to another joint bin; inside shots D stays below W*H
+    assert set(np.flatnonzero(gd > wl.width * wl.height).tolist()) == {57, 131, 198}
+
+
+@pytest.mark.parametrize("mode", ["uniform", "constant"])
+def test_joint_shotdiff_content_and_c2(mode):
+    wl = scn_synth.WORKLOADS["C2"]
+    pl = scn_harness.plan(wl)
+    gh, gd, rh, rd, _ = _joint_diff(wl, 8, 7001, 7009, mode=mode, pl=pl)
+    np.testing.assert_array_equal(gh, rh)
+    np.testing.assert_array_equal(gd, rd)
+
+
+def test_joint_shotdiff_errors():
+    wl = Workload("jderr", 8, 8, 1, 4, ("stride", 1), ("hist",))
+    job = scn_harness.DeviceJob(wl, 1, 4, with_halo=True)
+    H = torch.empty((3, 512), dtype=torch.int32, device="cuda")
+    D = torch.empty(3, dtype=torch.int32, device="cuda")
+    for j in (0, 9):
+        with pytest.raises(scn.ScnError) as e:
+            scn.scn_run_hist_shotdiff_joint(job.seq, 1, 4, j, H, D, H)
+        assert e.value.status == scn.SCN_EUNSUPPORTED
+    with pytest.raises(scn.ScnError) as e:  # position 1 needs its halo: no scratch given
+        scn.scn_run_hist_shotdiff_joint(job.seq, 1, 4, 4, H, D, None)
+    assert e.value.status == scn.SCN_EINVAL
+    scn.scn_run_hist_shotdiff_joint(job.seq, 2, 2, 4, H, D, None)  # empty range: no-op
+    job.close()
