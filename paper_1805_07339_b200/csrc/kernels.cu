@@ -50,6 +50,7 @@
 #include "ptx.cuh"
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -67,8 +68,10 @@ constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 p
 constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only kernels
 // kVarGen kernels: more warps hide the longer dependency chains of the realigned loads and
 // stores (measured, profiles/r02_tune_gen.jsonl: ds-only 1366x768 5.51 / 6.32 / 6.76 TB/s with
-// 8 / 12 / 16 warps; fused 4.12 / 4.96 / 4.92)
-constexpr int kGenDsWarps = 16;
+// 8 / 12 / 16 warps on the direct cross-lane stores; with the staged bulk stores 12 warps
+// are best, profiles/r02_tune_gen2.jsonl: 6.95 / 6.83 / 6.93 for 12 / 16 / 20). The fused
+// kernel takes 12 or 16 by its tile shape (fused_gen_warps).
+constexpr int kGenDsWarps = 12;
 constexpr int kGenFusedWarps = 12;
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
                                    // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
@@ -94,6 +97,7 @@ struct HistParams {
   int32_t joint;          // kModeJoint: J bins per channel (the output row holds J^3 counters)
   uint32_t tile;          // frame bytes per full tile (row-pair modes: rows_per_tile * W * 3)
   uint32_t slot;          // shared-memory bytes per ring slot (>= tile; + kGenSlack for kVarGen)
+  uint32_t out_off;       // kVarGen staged stores: offset of the slot's output stage (0 = direct stores)
   int32_t rows_per_tile;  // row-pair modes: rows per tile (even); 0 otherwise
   int32_t tpf;            // tiles per frame
   int64_t total_tiles;
@@ -173,6 +177,24 @@ __device__ __forceinline__ Layout make_layout_split(uint32_t base, uint32_t smem
   return L;
 }
 
+// Half-lane layout of the realigning fused kernel: the 64 KB key block at the first 64 KB
+// boundary above the control block, ring slots below and above it.
+__device__ __forceinline__ Layout make_layout_half(uint32_t base, uint32_t smem_bytes, uint32_t slot) {
+  Layout L;
+  L.ctrl = base;
+  const uint32_t end = base + smem_bytes;
+  L.table = (base + kCtrlBytes + 65535u) & ~65535u;
+  L.ring = (base + kCtrlBytes + 127) & ~127u;
+  L.stride = (slot + 127) & ~127u;
+  L.ring_hi = L.table + 65536u;
+  const int lo = L.table >= L.ring + slot ? (int)((L.table - L.ring - slot) / L.stride) + 1 : 0;
+  const int hi = end >= L.ring_hi + slot ? (int)((end - L.ring_hi - slot) / L.stride) + 1 : 0;
+  L.stages = lo + hi > kMaxStages ? kMaxStages : lo + hi;
+  L.n_lo = lo < L.stages ? lo : L.stages;
+  if (L.ring_hi > end) L.stages = 0;
+  return L;
+}
+
 template <int OFF>
 __device__ __forceinline__ void red_shared_add_off(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
@@ -202,10 +224,17 @@ __device__ __forceinline__ uint32_t pair_key_word(uint32_t a, uint32_t b) {
   asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(K) : "r"(b), "r"(a >> 4), "n"(0x0F0F0F0Fu));
   return K;
 }
-template <int K_, int I, bool H2>
+// Half-lane block (kHalf: the realigning fused kernel, H2 == 2): all three channels in one
+// 64 KB-aligned block of 256-byte key rows tab[key][c][lane / 2] (16 counters per channel, a
+// 64-byte spare), so every key takes ONE PRMT (key -> address byte 1, (lane / 2) << 2 in byte
+// 0, c * 64 as the ATOMS immediate). 64 KB instead of the split layout's 80 KB leaves the
+// ring 12-row tiles at 1366 wide (10 before): more bytes in flight per SM.
+template <int K_, int I, int H2>
 __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32_t lane4h) {
   constexpr int c = (4 * K_ + I) % 3;  // channel of byte 4*K_ + I
-  if constexpr (c < 2) {
+  if constexpr (H2 == 2) {
+    red_shared_add_off<c * 64>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
+  } else if constexpr (c < 2) {
     red_shared_add_off<c * 128>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
   } else if constexpr (H2) {  // split layout: tab2 | key << 6 | (lane / 2) << 2
     uint32_t x;
@@ -219,7 +248,7 @@ __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32
     red_shared_add_off<65536>(lop3_and_or<0xFFu << 7>(x, lane4));
   }
 }
-template <int K_, bool H2>
+template <int K_, int H2>
 __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uint32_t lane4h) {
   const uint32_t Kw = pair_key_word(w[K_], w[K_ + 6]);
   pair_key_step<K_, 0, H2>(Kw, lane4, lane4h);
@@ -227,7 +256,7 @@ __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uin
   pair_key_step<K_, 2, H2>(Kw, lane4, lane4h);
   pair_key_step<K_, 3, H2>(Kw, lane4, lane4h);
 }
-template <bool H2>
+template <int H2>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4, uint32_t lane4h = 0) {
   pair_word<0, H2>(w, lane4, lane4h); pair_word<1, H2>(w, lane4, lane4h); pair_word<2, H2>(w, lane4, lane4h);
   pair_word<3, H2>(w, lane4, lane4h); pair_word<4, H2>(w, lane4, lane4h); pair_word<5, H2>(w, lane4, lane4h);
@@ -430,6 +459,21 @@ __device__ __forceinline__ void st_global_24_any(uint8_t* dst, const uint32_t* o
   st_pred_u32(dst + (a2 - a), __funnelshift_r(o[0], o[1], 8u * (a2 - a)), hd && (a2 & 4u));
 }
 
+// 24 output bytes at ANY shared-memory address (kVarGen staged stores): the bytes up to the
+// next 4-byte boundary as a 1/2/4-byte head, five aligned words cut by one funnel shift each
+// (__funnelshift_rc: shift 32 = the high word, so m = 0 needs no special case), and the last
+// m bytes as a 1/2-byte tail — branch-free predicated stores, 8 at most, 5-7 executed.
+__device__ __forceinline__ void sts_24_any(uint32_t a, const uint32_t* o) {
+  const uint32_t m = a & 3u, sh = 8u * (4u - m), al = a + 4u - m;
+  sts_pred_u32(a, o[0], m == 0u);
+  sts_pred_u8(a, o[0], m & 1u);
+  sts_pred_u16(a + (m & 1u), o[0] >> (8u * (m & 1u)), m == 1u || m == 2u);
+#pragma unroll
+  for (int j = 0; j < 5; ++j) sts32(al + 4u * j, __funnelshift_rc(o[j], o[j + 1], sh));
+  sts_pred_u16(al + 20u, o[5] >> sh, m >= 2u);
+  sts_pred_u8(al + 20u + (m & 2u), o[5] >> 24, m & 1u);
+}
+
 // ---------------------------------------------------------------------------
 // The persistent TMA-ring kernel (modes: see the file header).
 // ---------------------------------------------------------------------------
@@ -440,12 +484,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr int kThreads = kConsThreads + 32;
   constexpr bool kRowPair = MODE == kModeFused || MODE == kModeDs;
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
-  constexpr bool kSplit = MODE == kModeFused;
+  constexpr bool kHalf = kGen && MODE == kModeFused;  // half-lane 64 KB block (see pair_key_step)
+  constexpr bool kSplit = MODE == kModeFused && !kHalf;
+  constexpr int kH2 = kHalf ? 2 : 1;
   constexpr bool kTable = MODE != kModeDs;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = smem_addr(smem);
-  Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.slot)
-                    : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
+  Layout L = kSplit  ? make_layout_split(base, p.smem_bytes, p.slot)
+             : kHalf ? make_layout_half(base, p.smem_bytes, p.slot)
+                     : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
                                   MODE == kModeRaw ? kRemapBytes : 0u);
   if (p.max_stages > 0 && L.stages > p.max_stages) {
     L.stages = p.max_stages;
@@ -476,8 +523,31 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
 
   const int64_t t0 = p.total_tiles * blockIdx.x / gridDim.x;
   const int64_t t1 = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
+  // kVarGen staged stores (contiguous output rows): each ring slot holds an input tile and,
+  // at out_off, the image of that tile's output bytes at the destination's alignment mod 16;
+  // the producer writes its 16-byte-aligned interior with one bulk store, the consumers write
+  // the < 16-byte head and tail fragments (shared with the neighbouring tiles) directly.
+  const bool kStaged = kGen && p.out_off != 0u;
+  const int64_t ow3 = (int64_t)(p.width / 2) * 3;
 
   if (warp == kConsWarps) {
+    // output tile (sitem, sk) of slot s: bytes [g0, g0 + n) of the destination frame
+    int64_t sitem = t0 / p.tpf;
+    int32_t sk = (int32_t)(t0 - sitem * p.tpf);
+    auto stage_store = [&](int ss, int64_t& it, int32_t& kk) {
+      if (it >= p.n_halo) {
+        const uint32_t rows = kk == p.tpf - 1 ? (uint32_t)(p.height - (p.tpf - 1) * p.rows_per_tile)
+                                              : (uint32_t)p.rows_per_tile;
+        const uint64_t g0 = (uint64_t)(uintptr_t)(p.ds_out + (it - p.n_halo) * (int64_t)(p.height / 2) * ow3 +
+                                                  (int64_t)kk * (p.rows_per_tile / 2) * ow3);
+        const uint64_t a = (g0 + 15) & ~15ull, b = (g0 + (uint64_t)(rows / 2) * (uint64_t)ow3) & ~15ull;
+        if (b > a) {
+          tma_store_1d(reinterpret_cast<void*>(a), L.slot(ss) + p.out_off + 16u, (uint32_t)(b - a));
+          bulk_commit();
+        }
+      }
+      if (++kk == p.tpf) { kk = 0; ++it; }
+    };
     // ---------------- producer: one elected lane issues the bulk copies ----------------
     if (lane == 0) {
       int s = 0;
@@ -492,6 +562,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       // per frame and BEFORE the empty-slot wait, so its latency overlaps the wait
       int64_t base_item = -1;
       uint64_t fbase = 0;
+      int defer = -1;  // kStaged: slot whose full-barrier arrive waits for the last store's read
       for (int64_t t = t0; t < t1; ++t, (++k == p.tpf) ? (k = 0, ++item) : 0) {
         const uint64_t off = (uint64_t)k * p.tile;
         const uint64_t len = (uint64_t)p.F - off < p.tile ? (uint64_t)p.F - off : p.tile;
@@ -515,9 +586,45 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         const uint32_t bytes = (uint32_t)(((fbase + off + len + 15) & ~15ull) - a0);
         if (p.prod_sleep) mbar_wait_sleep(empty0 + 8 * s, ph ^ 1, p.prod_sleep);
         else mbar_wait(empty0 + 8 * s, ph ^ 1);
-        mbar_arrive_expect_tx(full0 + 8 * s, bytes);
-        tma_load_1d(L.slot(s), reinterpret_cast<const void*>(a0), bytes, full0 + 8 * s);
+        if (kStaged) {
+          // The consumers released slot s: store the output tile they staged in it and load the
+          // next input tile into the slot's input region. The consumers may rewrite the output
+          // region only after the store has READ it, so the slot's full-barrier arrive waits for
+          // that — deferred to the next iteration (a consumer tile later, after the next empty
+          // wait), where the read is long done, so the producer never blocks on its own store.
+          if (defer >= 0) {
+            bulk_wait_read0();
+            mbar_arrive(full0 + 8 * defer);
+            defer = -1;
+          }
+          const bool st_out = t - t0 >= L.stages;
+          if (st_out) stage_store(s, sitem, sk);
+          mbar_expect_tx(full0 + 8 * s, bytes);
+          tma_load_1d(L.slot(s), reinterpret_cast<const void*>(a0), bytes, full0 + 8 * s);
+          if (st_out) defer = s;
+          else mbar_arrive(full0 + 8 * s);
+        } else {
+          mbar_arrive_expect_tx(full0 + 8 * s, bytes);
+          tma_load_1d(L.slot(s), reinterpret_cast<const void*>(a0), bytes, full0 + 8 * s);
+        }
         if (++s == L.stages) { s = 0; ph ^= 1; }
+      }
+      if (kStaged) {  // the last min(stages, tiles) output tiles
+        if (defer >= 0) {
+          bulk_wait_read0();
+          mbar_arrive(full0 + 8 * defer);
+        }
+        const int64_t nt = t1 - t0;
+        if (nt < L.stages) {  // slots 0 .. nt-1 hold their first tiles (phase 0)
+          s = 0;
+          ph = 1;
+        }
+        for (int64_t t = nt > L.stages ? nt - L.stages : 0; t < nt; ++t) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          stage_store(s, sitem, sk);
+          if (++s == L.stages) { s = 0; ph ^= 1; }
+        }
+        bulk_wait0();
       }
     }
     return;
@@ -526,7 +633,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // ---------------- consumers ----------------
   const int ctid = threadIdx.x;  // 0 .. kConsThreads-1
   // split layout: channels 0/1 in the 64 KB block after tab2, channel 2 in tab2 (half lanes)
-  const uint32_t lane4 = (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
+  const uint32_t lane4 = kHalf ? L.table | ((uint32_t)lane >> 1 << 2)
+                              : (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
   const uint32_t lane4h = L.table | ((uint32_t)lane >> 1 << 2);
   int s = 0;
   uint32_t ph = 0;
@@ -605,7 +713,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         uint32_t sum = 0;
-        if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
+        if (kHalf) {  // tab[key][c]: 64-byte half-lane rows in 256-byte key rows
+          const uint32_t ra = L.table + key * 256u + c * 64u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 v = lds128(ra + (uint32_t)(((j + r) & 3) * 16));
+            sum += v.x + v.y + v.z + v.w;
+          }
+        } else if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
           const uint32_t ra = L.table + key * 64u;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -712,7 +827,42 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       const uint32_t npairs = (rows / 2) * rg.upr;
       uint8_t* dsf = (item >= p.n_halo) ? rg.ds_frame + (int64_t)k * rg.tile_out : nullptr;
       uint32_t u = ucur, rp = rpc, xc = xcc;
-      if constexpr (kGen) {
+      // staged stores: tile-local output byte c goes to the stage at ob + c if c is in the
+      // bulk-stored interior [hl, tb), else straight to dsf[c] (the fragments, < 16 B each)
+      uint32_t ob = 0, hl = 0, tb = 0;
+      if (kStaged && dsf) {
+        const uint32_t n = (rows / 2) * (uint32_t)ow3, r = (uint32_t)(uintptr_t)dsf & 15u;
+        hl = (16u - r) & 15u;
+        tb = (uint32_t)((((uint64_t)(uintptr_t)dsf + n) & ~15ull) - (uint64_t)(uintptr_t)dsf);
+        if (tb <= hl) hl = tb = n;  // no aligned interior: every byte direct
+        ob = L.slot(s) + p.out_off + 16u - hl;
+      }
+      auto put_byte = [&](uint32_t c, uint32_t v) {
+        if (c >= hl && c < tb) sts_u8(ob + c, v);
+        else dsf[c] = (uint8_t)v;
+      };
+      if (kStaged) {
+        for (; u < npairs; u += kConsThreads, rp += rg.dq, xc += rg.dr, (xc >= rg.upr) ? (xc -= rg.upr, ++rp) : 0) {
+          const uint32_t a = slot + rp * 2u * rg.rowb + xc * 48u;
+          uint32_t wt[12], wb[12], o[6];
+          load_unit_any(a, wt);
+          load_unit_any(a + rg.rowb, wb);
+          if constexpr (MODE == kModeFused) {
+            hist_unit_pair<kH2>(wt, lane4, lane4h);
+            hist_unit_pair<kH2>(wb, lane4, lane4h);
+          }
+          if (dsf) {
+            ds_unit(wt, wb, o);
+            const uint32_t c = rp * (uint32_t)ow3 + xc * 24u;
+            if (c >= hl && c + 24u <= tb) {
+              sts_24_any(ob + c, o);
+            } else {  // a fragment edge of the tile (two chunks per tile at most)
+#pragma unroll
+              for (int q = 0; q < 24; ++q) put_byte(c + (uint32_t)q, o[q >> 2] >> (8 * (q & 3)));
+            }
+          }
+        }
+      } else if constexpr (kGen) {
         // Warp-uniform iterations (the shuffles of the realigned stores need every lane): a lane
         // whose units of this tile are done idles without advancing, so the carried (u, rp, xc)
         // are exactly the per-lane loop's. Lanes hold consecutive units except where the
@@ -727,8 +877,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             load_unit_any(a, wt);
             load_unit_any(a + rg.rowb, wb);
             if constexpr (MODE == kModeFused) {
-              hist_unit_pair<true>(wt, lane4, lane4h);
-              hist_unit_pair<true>(wb, lane4, lane4h);
+              hist_unit_pair<kH2>(wt, lane4, lane4h);
+              hist_unit_pair<kH2>(wb, lane4, lane4h);
             }
             if (dsf) ds_unit(wt, wb, o);
           }
@@ -752,8 +902,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit(a, wt);
           load_unit(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<true>(wt, lane4, lane4h);
-            hist_unit_pair<true>(wb, lane4, lane4h);
+            hist_unit_pair<kH2>(wt, lane4, lane4h);
+            hist_unit_pair<kH2>(wb, lane4, lane4h);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -780,7 +930,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             for (uint32_t y = rg.oq, j = rg.orr; y < rows / 2; y += rg.odq, j += rg.odr, (j >= rg.tob) ? (j -= rg.tob, ++y) : 0) {
               const uint32_t i0 = slot + 2u * y * rg.rowb + 48u * rg.upr + 2u * (j - j % 3u) + j % 3u;
               const uint32_t sum = lds_u8(i0) + lds_u8(i0 + 3) + lds_u8(i0 + rg.rowb) + lds_u8(i0 + rg.rowb + 3);
-              dsf[(int64_t)y * rg.pitch + 24 * rg.upr + j] = (uint8_t)((sum + 2u) >> 2);
+              if (kStaged) put_byte(y * (uint32_t)ow3 + 24u * rg.upr + j, (sum + 2u) >> 2);
+              else dsf[(int64_t)y * rg.pitch + 24 * rg.upr + j] = (uint8_t)((sum + 2u) >> 2);
             }
           }
         }
@@ -790,7 +941,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           uint32_t w[12];
           if constexpr (kGen) load_unit_any(slot + (rows - 1) * rg.rowb + v * 48u, w);
           else load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
-          hist_unit_pair<true>(w, lane4, lane4h);
+          hist_unit_pair<kH2>(w, lane4, lane4h);
         }
       }
     } else {
@@ -847,6 +998,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       }
       ucur = u - nunits;
     }
+    if (kStaged) fence_proxy_async_smem();  // staged output bytes -> the producer's bulk store
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
     if (++s == L.stages) { s = 0; ph ^= 1; }
@@ -967,6 +1119,9 @@ struct Knobs {
   int l2_prefetch_hist = 0;   //   (the read-only histogram keeps 0: the data would cross L2 twice)
   uint32_t prod_sleep = 0;    // SCN_PROD_SLEEP: producer empty-slot wait suspend hint in ns (0 = spin)
   int hist_warps = 0;         // SCN_HIST_WARPS: consumer warps of the hist-only kernels (tuning build: 8/20)
+  int gen_stage = 1;          // SCN_GEN_STAGE: kVarGen downsample-only output through the staged bulk
+                              // store (0 = the direct cross-lane stores, kept for montage canvases;
+                              // 2 = the fused kernel staged too)
   int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
                               // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
@@ -990,6 +1145,7 @@ static void read_knobs_once() {
   if (pf >= 0) k.l2_prefetch_fused = k.l2_prefetch_hist = pf;
   k.prod_sleep = (uint32_t)env_int("SCN_PROD_SLEEP", 0);
   k.gen_warps = env_int("SCN_GEN_WARPS", 0);
+  k.gen_stage = env_int("SCN_GEN_STAGE", 1);
   k.hist_warps = env_int("SCN_HIST_WARPS", 0);
   g_knobs = k;
 }
@@ -1039,15 +1195,33 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Consumer warps of the fused kVarGen kernel: its warp-uniform loop (the cross-lane stores)
+// runs ceil(x) iterations per warp and tile for x = unit pairs per consumer thread, so a warp's
+// lanes are busy x / ceil(x) of the time; take the count (12 or 16) with the higher ratio.
+// Measured (profiles/r02_tune_gen2.jsonl): 1366x768 12 -> 16 warps +9 % (x = 1.33 -> 1.00),
+// 854x480 +0.6 % (1.24 -> 0.93), 426x240 16 warps -8 % (1.35 -> 1.02, ratio 0.51): 12 kept.
+static int fused_gen_warps(const HistParams& p) {
+  const double units = (double)(p.rows_per_tile / 2) * (double)(p.width / 16);
+  auto busy = [&](int nw) {
+    const double x = units / (32.0 * nw);
+    return x <= 0 ? 0.0 : x / std::ceil(x);
+  };
+  return busy(16) > busy(12) ? 16 : 12;
+}
+
 // The kVarGen kernels (any width / output alignment) at the knob's warp count.
 template <int MODE>
 static cudaError_t launch_gen(const HistParams& p, cudaStream_t st) {
   constexpr int kW = MODE == kModeDs ? kGenDsWarps : kGenFusedWarps;
+  if constexpr (MODE == kModeFused)
+    if (knobs().gen_warps == 0 && fused_gen_warps(p) == 16) return launch_tma<MODE, 16, kVarGen>(p, st);
 #ifdef SCN_TUNING
   const int w = knobs().gen_warps;
   if (w == 8 && kW != 8) return launch_tma<MODE, 8, kVarGen>(p, st);
   if (w == 12 && kW != 12) return launch_tma<MODE, 12, kVarGen>(p, st);
   if (w == 16 && kW != 16) return launch_tma<MODE, 16, kVarGen>(p, st);
+  if (w == 20 && kW != 20) return launch_tma<MODE, 20, kVarGen>(p, st);
+  if (w == 24 && kW != 24) return launch_tma<MODE, 24, kVarGen>(p, st);
 #endif
   return launch_tma<MODE, kW, kVarGen>(p, st);
 }
@@ -1055,11 +1229,30 @@ static cudaError_t launch_gen(const HistParams& p, cudaStream_t st) {
 // Rows per row-pair tile of the downsample-only kernel: the largest even row count whose
 // slots give 4 ring stages (1080p: 8 rows; run with 3 of them), or 2 stages if that is
 // under 4 rows; 0 if not even 2 rows fit twice. An explicit tile size (knob) wins.
-static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile) {
+// Ring-slot bytes of a row-pair tile of r rows: the input rows (+ kGenSlack for kVarGen) and,
+// for kVarGen staged stores, the output stage at out_off = ceil16(input) holding the tile's
+// r/2 output rows after a 16-byte lead (the head fragment's place, never written).
+static uint32_t stage_off(int r, int64_t rowb, uint32_t slack) {
+  return (uint32_t)(((int64_t)r * rowb + slack + 15) & ~15ll);
+}
+static uint32_t slot_bytes(int r, int64_t rowb, uint32_t slack, bool staged) {
+  const int64_t in = (int64_t)r * rowb + slack;
+  if (!staged) return (uint32_t)in;
+  return stage_off(r, rowb, slack) + 16u + (uint32_t)((((int64_t)(r / 2) * (rowb / 6) * 3) + 15) & ~15ll);
+}
+
+static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged) {
   if (env_tile) return (int)((int64_t)env_tile / rowb) & ~1;
   const int64_t ring = (int64_t)g_smem_optin - (int64_t)kCtrlBytes - 2048;
-  int r = (int)((ring / 4 - slack) / rowb) & ~1;
-  if (r < 4) r = (int)((ring / 2 - slack) / rowb) & ~1;
+  // round 1 sized the input tile at a quarter of the ring; a staged slot (input + output
+  // stage, 1.25x) keeps that input size within a third (the ring runs 3 stages)
+  const int64_t cap = staged ? ring / 3 : ring / 4;
+  int r = (int)((cap - slack) / rowb) & ~1;
+  while (r >= 2 && (int64_t)slot_bytes(r, rowb, slack, staged) > cap) r -= 2;
+  if (r < 4) {
+    r = (int)((ring / 2 - slack) / rowb) & ~1;
+    while (r >= 2 && (int64_t)slot_bytes(r, rowb, slack, staged) > ring / 2) r -= 2;
+  }
   return r < 2 ? 0 : r;
 }
 
@@ -1067,13 +1260,14 @@ static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile) {
 // smem base = the per-block reserved size): the largest even row count (tile <= 64 KB)
 // whose slots give >= 3 ring stages over the two ring segments; 0 if none. The device
 // recomputes the same layout and traps on < 2 stages.
-static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile) {
+static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged, bool half) {
   const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin;
-  const uint32_t block = (base + kCtrlBytes + kTab2Bytes + 65535u) & ~65535u;
-  const uint32_t tab2 = block - kTab2Bytes, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
+  const uint32_t t2 = half ? 0u : kTab2Bytes;  // make_layout_half: no tab2 below the block
+  const uint32_t block = (base + kCtrlBytes + t2 + 65535u) & ~65535u;
+  const uint32_t tab2 = block - t2, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
   if (hi > end) return 0;
   auto stages = [&](int r) {
-    const uint32_t slot = (uint32_t)(r * rowb) + slack, stride = (slot + 127u) & ~127u;
+    const uint32_t slot = slot_bytes(r, rowb, slack, staged), stride = (slot + 127u) & ~127u;
     const int lo = tab2 >= ring + slot ? (int)((tab2 - ring - slot) / stride) + 1 : 0;
     const int up = end >= hi + slot ? (int)((end - hi - slot) / stride) + 1 : 0;
     return lo + up;
@@ -1093,6 +1287,11 @@ static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile) 
 // and 8-byte aligned output units (pitch and base multiples of 8); anything else takes kVarGen.
 static bool rowpair_aligned(int32_t width, int64_t pitch, const uint8_t* out) {
   return width % 16 == 0 && pitch % 8 == 0 && ((uintptr_t)out & 7u) == 0;
+}
+
+// kVarGen staged stores need each tile's output rows contiguous (no montage canvas pitch)
+static bool staged_ok(int32_t width, int64_t pitch, int32_t ds_cols) {
+  return ds_cols == 0 && pitch == (int64_t)(width / 2) * 3 && knobs().gen_stage != 0;
 }
 
 static HistParams base_params(const HistJob& j) {
@@ -1179,12 +1378,14 @@ cudaError_t launch_histogram_joint(const HistJob& j, cudaStream_t st, int* launc
 }
 
 // Row-pair tiling of frames for the fused / downsample-only kernels.
-static void rowpair_tiles(HistParams& p, int rpt, bool gen) {
+static void rowpair_tiles(HistParams& p, int rpt, bool gen, bool staged) {
   const int64_t rowb = (int64_t)p.width * 3;
   if (rpt > p.height) rpt = p.height + (p.height & 1);  // whole frame in one tile
   p.rows_per_tile = rpt;
   p.tile = (uint32_t)(rpt * rowb);
-  p.slot = p.tile + (gen ? kGenSlack : 0u);
+  const uint32_t slack = gen ? kGenSlack : 0u;
+  p.slot = slot_bytes(rpt, rowb, slack, staged);
+  p.out_off = staged ? stage_off(rpt, rowb, slack) : 0u;
   p.tpf = (p.height + rpt - 1) / rpt;
   p.total_tiles = p.n_items * p.tpf;
   p.l2_prefetch = knobs().l2_prefetch_fused;
@@ -1197,7 +1398,8 @@ cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int
   if (e != cudaSuccess) return e;
   if (n <= 0 || width < 2 || height < 2) return cudaSuccess;
   const bool gen = !rowpair_aligned(width, pitch, out);
-  const int rpt = rows_per_tile_ds((int64_t)width * 3, gen ? kGenSlack : 0u, knobs().ds_tile);
+  const bool staged = gen && staged_ok(width, pitch, ds_cols);
+  const int rpt = rows_per_tile_ds((int64_t)width * 3, gen ? kGenSlack : 0u, knobs().ds_tile, staged);
   *launches += 1;
   if (rpt < 2) {  // rows too wide for a ring slot
     const int64_t rows = n * (height / 2);
@@ -1215,7 +1417,7 @@ cudaError_t launch_downsample(const FrameSrc& src, int64_t n, int32_t width, int
   j.height = height;
   j.bins = 16;
   HistParams p = base_params(j);
-  rowpair_tiles(p, rpt, gen);
+  rowpair_tiles(p, rpt, gen, staged);
   p.l2_prefetch = 0;  // measured: the downsample-only kernel keeps 0
   p.table_bytes = 0;
   p.table_align = 128;
@@ -1228,7 +1430,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   if (j.n_items <= 0) return cudaSuccess;
   const int64_t pitch = j.ds_pitch > 0 ? j.ds_pitch : (int64_t)(j.width / 2) * 3;
   const bool gen = !rowpair_aligned(j.width, pitch, j.ds_out);
-  const int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile);
+  // the realigning fused kernel keeps direct stores: its ring slots are worth more as input
+  // (a staged slot would cost two rows per tile; measured slower, DESIGN.md §5 kVarGen)
+  const bool staged = gen && knobs().gen_stage == 2 && staged_ok(j.width, pitch, j.ds_cols);  // tuning A/B only
+  const int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged, gen);
   const bool fused = divides16(j.bins) && hist_impl() == 0 && rpt >= 2 && j.n_halo == 0 && j.width >= 2 &&
                      j.height >= 2;
   if (!fused) {  // two passes: histogram, then downsample
@@ -1243,8 +1448,8 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
                              j.ds_cols);
   }
   HistParams p = base_params(j);
-  rowpair_tiles(p, rpt, gen);
-  p.table_bytes = kTab2Bytes + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
+  rowpair_tiles(p, rpt, gen, staged);
+  p.table_bytes = gen ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
   return gen ? launch_gen<kModeFused>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
