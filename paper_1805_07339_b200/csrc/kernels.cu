@@ -50,7 +50,6 @@
 #include "ptx.cuh"
 
 #include <atomic>
-#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -69,8 +68,7 @@ constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only
 // kVarGen kernels: more warps hide the longer dependency chains of the realigned loads and
 // stores (measured, profiles/r02_tune_gen.jsonl: ds-only 1366x768 5.51 / 6.32 / 6.76 TB/s with
 // 8 / 12 / 16 warps on the direct cross-lane stores; with the staged bulk stores 12 warps
-// are best, profiles/r02_tune_gen2.jsonl: 6.95 / 6.83 / 6.93 for 12 / 16 / 20). The fused
-// kernel takes 12 or 16 by its tile shape (fused_gen_warps).
+// are best, profiles/r02_tune_gen2.jsonl: 6.95 / 6.83 / 6.93 for 12 / 16 / 20).
 constexpr int kGenDsWarps = 12;
 constexpr int kGenFusedWarps = 12;
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
@@ -177,24 +175,6 @@ __device__ __forceinline__ Layout make_layout_split(uint32_t base, uint32_t smem
   return L;
 }
 
-// Half-lane layout of the realigning fused kernel: the 64 KB key block at the first 64 KB
-// boundary above the control block, ring slots below and above it.
-__device__ __forceinline__ Layout make_layout_half(uint32_t base, uint32_t smem_bytes, uint32_t slot) {
-  Layout L;
-  L.ctrl = base;
-  const uint32_t end = base + smem_bytes;
-  L.table = (base + kCtrlBytes + 65535u) & ~65535u;
-  L.ring = (base + kCtrlBytes + 127) & ~127u;
-  L.stride = (slot + 127) & ~127u;
-  L.ring_hi = L.table + 65536u;
-  const int lo = L.table >= L.ring + slot ? (int)((L.table - L.ring - slot) / L.stride) + 1 : 0;
-  const int hi = end >= L.ring_hi + slot ? (int)((end - L.ring_hi - slot) / L.stride) + 1 : 0;
-  L.stages = lo + hi > kMaxStages ? kMaxStages : lo + hi;
-  L.n_lo = lo < L.stages ? lo : L.stages;
-  if (L.ring_hi > end) L.stages = 0;
-  return L;
-}
-
 template <int OFF>
 __device__ __forceinline__ void red_shared_add_off(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
@@ -224,17 +204,10 @@ __device__ __forceinline__ uint32_t pair_key_word(uint32_t a, uint32_t b) {
   asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(K) : "r"(b), "r"(a >> 4), "n"(0x0F0F0F0Fu));
   return K;
 }
-// Half-lane block (kHalf: the realigning fused kernel, H2 == 2): all three channels in one
-// 64 KB-aligned block of 256-byte key rows tab[key][c][lane / 2] (16 counters per channel, a
-// 64-byte spare), so every key takes ONE PRMT (key -> address byte 1, (lane / 2) << 2 in byte
-// 0, c * 64 as the ATOMS immediate). 64 KB instead of the split layout's 80 KB leaves the
-// ring 12-row tiles at 1366 wide (10 before): more bytes in flight per SM.
-template <int K_, int I, int H2>
+template <int K_, int I, bool H2>
 __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32_t lane4h) {
   constexpr int c = (4 * K_ + I) % 3;  // channel of byte 4*K_ + I
-  if constexpr (H2 == 2) {
-    red_shared_add_off<c * 64>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
-  } else if constexpr (c < 2) {
+  if constexpr (c < 2) {
     red_shared_add_off<c * 128>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
   } else if constexpr (H2) {  // split layout: tab2 | key << 6 | (lane / 2) << 2
     uint32_t x;
@@ -248,7 +221,7 @@ __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32
     red_shared_add_off<65536>(lop3_and_or<0xFFu << 7>(x, lane4));
   }
 }
-template <int K_, int H2>
+template <int K_, bool H2>
 __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uint32_t lane4h) {
   const uint32_t Kw = pair_key_word(w[K_], w[K_ + 6]);
   pair_key_step<K_, 0, H2>(Kw, lane4, lane4h);
@@ -256,7 +229,7 @@ __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uin
   pair_key_step<K_, 2, H2>(Kw, lane4, lane4h);
   pair_key_step<K_, 3, H2>(Kw, lane4, lane4h);
 }
-template <int H2>
+template <bool H2>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4, uint32_t lane4h = 0) {
   pair_word<0, H2>(w, lane4, lane4h); pair_word<1, H2>(w, lane4, lane4h); pair_word<2, H2>(w, lane4, lane4h);
   pair_word<3, H2>(w, lane4, lane4h); pair_word<4, H2>(w, lane4, lane4h); pair_word<5, H2>(w, lane4, lane4h);
@@ -484,15 +457,12 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr int kThreads = kConsThreads + 32;
   constexpr bool kRowPair = MODE == kModeFused || MODE == kModeDs;
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
-  constexpr bool kHalf = kGen && MODE == kModeFused;  // half-lane 64 KB block (see pair_key_step)
-  constexpr bool kSplit = MODE == kModeFused && !kHalf;
-  constexpr int kH2 = kHalf ? 2 : 1;
+  constexpr bool kSplit = MODE == kModeFused;
   constexpr bool kTable = MODE != kModeDs;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = smem_addr(smem);
-  Layout L = kSplit  ? make_layout_split(base, p.smem_bytes, p.slot)
-             : kHalf ? make_layout_half(base, p.smem_bytes, p.slot)
-                     : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
+  Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.slot)
+                    : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
                                   MODE == kModeRaw ? kRemapBytes : 0u);
   if (p.max_stages > 0 && L.stages > p.max_stages) {
     L.stages = p.max_stages;
@@ -633,8 +603,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // ---------------- consumers ----------------
   const int ctid = threadIdx.x;  // 0 .. kConsThreads-1
   // split layout: channels 0/1 in the 64 KB block after tab2, channel 2 in tab2 (half lanes)
-  const uint32_t lane4 = kHalf ? L.table | ((uint32_t)lane >> 1 << 2)
-                              : (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
+  const uint32_t lane4 = (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
   const uint32_t lane4h = L.table | ((uint32_t)lane >> 1 << 2);
   int s = 0;
   uint32_t ph = 0;
@@ -713,14 +682,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         uint32_t sum = 0;
-        if (kHalf) {  // tab[key][c]: 64-byte half-lane rows in 256-byte key rows
-          const uint32_t ra = L.table + key * 256u + c * 64u;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 v = lds128(ra + (uint32_t)(((j + r) & 3) * 16));
-            sum += v.x + v.y + v.z + v.w;
-          }
-        } else if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
+        if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
           const uint32_t ra = L.table + key * 64u;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -848,8 +810,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit_any(a, wt);
           load_unit_any(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<kH2>(wt, lane4, lane4h);
-            hist_unit_pair<kH2>(wb, lane4, lane4h);
+            hist_unit_pair<true>(wt, lane4, lane4h);
+            hist_unit_pair<true>(wb, lane4, lane4h);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -877,8 +839,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             load_unit_any(a, wt);
             load_unit_any(a + rg.rowb, wb);
             if constexpr (MODE == kModeFused) {
-              hist_unit_pair<kH2>(wt, lane4, lane4h);
-              hist_unit_pair<kH2>(wb, lane4, lane4h);
+              hist_unit_pair<true>(wt, lane4, lane4h);
+              hist_unit_pair<true>(wb, lane4, lane4h);
             }
             if (dsf) ds_unit(wt, wb, o);
           }
@@ -902,8 +864,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit(a, wt);
           load_unit(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<kH2>(wt, lane4, lane4h);
-            hist_unit_pair<kH2>(wb, lane4, lane4h);
+            hist_unit_pair<true>(wt, lane4, lane4h);
+            hist_unit_pair<true>(wb, lane4, lane4h);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -941,7 +903,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           uint32_t w[12];
           if constexpr (kGen) load_unit_any(slot + (rows - 1) * rg.rowb + v * 48u, w);
           else load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
-          hist_unit_pair<kH2>(w, lane4, lane4h);
+          hist_unit_pair<true>(w, lane4, lane4h);
         }
       }
     } else {
@@ -1195,26 +1157,10 @@ static cudaError_t launch_tma(HistParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Consumer warps of the fused kVarGen kernel: its warp-uniform loop (the cross-lane stores)
-// runs ceil(x) iterations per warp and tile for x = unit pairs per consumer thread, so a warp's
-// lanes are busy x / ceil(x) of the time; take the count (12 or 16) with the higher ratio.
-// Measured (profiles/r02_tune_gen2.jsonl): 1366x768 12 -> 16 warps +9 % (x = 1.33 -> 1.00),
-// 854x480 +0.6 % (1.24 -> 0.93), 426x240 16 warps -8 % (1.35 -> 1.02, ratio 0.51): 12 kept.
-static int fused_gen_warps(const HistParams& p) {
-  const double units = (double)(p.rows_per_tile / 2) * (double)(p.width / 16);
-  auto busy = [&](int nw) {
-    const double x = units / (32.0 * nw);
-    return x <= 0 ? 0.0 : x / std::ceil(x);
-  };
-  return busy(16) > busy(12) ? 16 : 12;
-}
-
 // The kVarGen kernels (any width / output alignment) at the knob's warp count.
 template <int MODE>
 static cudaError_t launch_gen(const HistParams& p, cudaStream_t st) {
   constexpr int kW = MODE == kModeDs ? kGenDsWarps : kGenFusedWarps;
-  if constexpr (MODE == kModeFused)
-    if (knobs().gen_warps == 0 && fused_gen_warps(p) == 16) return launch_tma<MODE, 16, kVarGen>(p, st);
 #ifdef SCN_TUNING
   const int w = knobs().gen_warps;
   if (w == 8 && kW != 8) return launch_tma<MODE, 8, kVarGen>(p, st);
@@ -1260,11 +1206,10 @@ static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile, boo
 // smem base = the per-block reserved size): the largest even row count (tile <= 64 KB)
 // whose slots give >= 3 ring stages over the two ring segments; 0 if none. The device
 // recomputes the same layout and traps on < 2 stages.
-static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged, bool half) {
+static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged) {
   const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin;
-  const uint32_t t2 = half ? 0u : kTab2Bytes;  // make_layout_half: no tab2 below the block
-  const uint32_t block = (base + kCtrlBytes + t2 + 65535u) & ~65535u;
-  const uint32_t tab2 = block - t2, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
+  const uint32_t block = (base + kCtrlBytes + kTab2Bytes + 65535u) & ~65535u;
+  const uint32_t tab2 = block - kTab2Bytes, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
   if (hi > end) return 0;
   auto stages = [&](int r) {
     const uint32_t slot = slot_bytes(r, rowb, slack, staged), stride = (slot + 127u) & ~127u;
@@ -1433,7 +1378,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   // the realigning fused kernel keeps direct stores: its ring slots are worth more as input
   // (a staged slot would cost two rows per tile; measured slower, DESIGN.md §5 kVarGen)
   const bool staged = gen && knobs().gen_stage == 2 && staged_ok(j.width, pitch, j.ds_cols);  // tuning A/B only
-  const int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged, gen);
+  const int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged);
   const bool fused = divides16(j.bins) && hist_impl() == 0 && rpt >= 2 && j.n_halo == 0 && j.width >= 2 &&
                      j.height >= 2;
   if (!fused) {  // two passes: histogram, then downsample
@@ -1449,7 +1394,7 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   }
   HistParams p = base_params(j);
   rowpair_tiles(p, rpt, gen, staged);
-  p.table_bytes = gen ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
+  p.table_bytes = kTab2Bytes + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
   return gen ? launch_gen<kModeFused>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
