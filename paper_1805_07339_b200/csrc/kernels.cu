@@ -61,7 +61,8 @@ namespace scn {
 enum : int {
   kModePair = 0, kModeFused = 2, kModeDs = 3, kModeRaw = 4, kModeMatch = 5, kModeMatchPacked = 6, kModeJoint = 7
 };
-constexpr int kVarGen = 1;  // row-pair modes: any width / output alignment
+constexpr int kVarGen = 1;   // row-pair modes: any width / output alignment
+constexpr int kVarHalf = 2;  // fused kVarGen: half-lane 64 KB key block (see pair_key_step)
 
 constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 producer warp)
 constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only kernels
@@ -71,6 +72,7 @@ constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only
 // are best, profiles/r02_tune_gen2.jsonl: 6.95 / 6.83 / 6.93 for 12 / 16 / 20).
 constexpr int kGenDsWarps = 12;
 constexpr int kGenFusedWarps = 12;
+constexpr int kGenHalfWarps = 16;  // half-lane fused kernel (1366x768: 12 rows x 85 units = 510 unit pairs per tile)
 constexpr uint32_t kTile = 43008;  // 896 x 48 bytes: a multiple of 48 (channel phase) and 16 (TMA); 3 stages.
                                    // Measured best of 24,576..64,512 on B200 (profiles/r01_tune.jsonl)
 constexpr uint32_t kGenSlack = 64;  // kVarGen slots: 15 B of leading misalignment + 15 B rounding + 16 B overread
@@ -175,6 +177,24 @@ __device__ __forceinline__ Layout make_layout_split(uint32_t base, uint32_t smem
   return L;
 }
 
+// Half-lane layout of the realigning fused kernel: the 64 KB key block at the first 64 KB
+// boundary above the control block, ring slots below and above it.
+__device__ __forceinline__ Layout make_layout_half(uint32_t base, uint32_t smem_bytes, uint32_t slot) {
+  Layout L;
+  L.ctrl = base;
+  const uint32_t end = base + smem_bytes;
+  L.table = (base + kCtrlBytes + 65535u) & ~65535u;
+  L.ring = (base + kCtrlBytes + 127) & ~127u;
+  L.stride = (slot + 127) & ~127u;
+  L.ring_hi = L.table + 65536u;
+  const int lo = L.table >= L.ring + slot ? (int)((L.table - L.ring - slot) / L.stride) + 1 : 0;
+  const int hi = end >= L.ring_hi + slot ? (int)((end - L.ring_hi - slot) / L.stride) + 1 : 0;
+  L.stages = lo + hi > kMaxStages ? kMaxStages : lo + hi;
+  L.n_lo = lo < L.stages ? lo : L.stages;
+  if (L.ring_hi > end) L.stages = 0;
+  return L;
+}
+
 template <int OFF>
 __device__ __forceinline__ void red_shared_add_off(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
@@ -204,10 +224,17 @@ __device__ __forceinline__ uint32_t pair_key_word(uint32_t a, uint32_t b) {
   asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(K) : "r"(b), "r"(a >> 4), "n"(0x0F0F0F0Fu));
   return K;
 }
-template <int K_, int I, bool H2>
+// Half-lane block (H2 == 2, the realigning fused kernel when it buys a bigger tile): all
+// three channels in one 64 KB-aligned block of 256-byte key rows tab[key][c][lane / 2] (16
+// counters per channel, a 64-byte spare), so every key takes ONE PRMT (key -> address byte 1,
+// (lane / 2) << 2 in byte 0, c * 64 as the ATOMS immediate). 64 KB instead of the split
+// layout's 80 KB: at 1366 wide the ring takes 12-row tiles instead of 10.
+template <int K_, int I, int H2>
 __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32_t lane4h) {
   constexpr int c = (4 * K_ + I) % 3;  // channel of byte 4*K_ + I
-  if constexpr (c < 2) {
+  if constexpr (H2 == 2) {
+    red_shared_add_off<c * 64>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
+  } else if constexpr (c < 2) {
     red_shared_add_off<c * 128>(__byte_perm(K, lane4, 0x7604u | (I << 4)));
   } else if constexpr (H2) {  // split layout: tab2 | key << 6 | (lane / 2) << 2
     uint32_t x;
@@ -221,7 +248,7 @@ __device__ __forceinline__ void pair_key_step(uint32_t K, uint32_t lane4, uint32
     red_shared_add_off<65536>(lop3_and_or<0xFFu << 7>(x, lane4));
   }
 }
-template <int K_, bool H2>
+template <int K_, int H2>
 __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uint32_t lane4h) {
   const uint32_t Kw = pair_key_word(w[K_], w[K_ + 6]);
   pair_key_step<K_, 0, H2>(Kw, lane4, lane4h);
@@ -229,7 +256,7 @@ __device__ __forceinline__ void pair_word(const uint32_t* w, uint32_t lane4, uin
   pair_key_step<K_, 2, H2>(Kw, lane4, lane4h);
   pair_key_step<K_, 3, H2>(Kw, lane4, lane4h);
 }
-template <bool H2>
+template <int H2>
 __device__ __forceinline__ void hist_unit_pair(const uint32_t* w, uint32_t lane4, uint32_t lane4h = 0) {
   pair_word<0, H2>(w, lane4, lane4h); pair_word<1, H2>(w, lane4, lane4h); pair_word<2, H2>(w, lane4, lane4h);
   pair_word<3, H2>(w, lane4, lane4h); pair_word<4, H2>(w, lane4, lane4h); pair_word<5, H2>(w, lane4, lane4h);
@@ -457,12 +484,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr int kThreads = kConsThreads + 32;
   constexpr bool kRowPair = MODE == kModeFused || MODE == kModeDs;
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
-  constexpr bool kSplit = MODE == kModeFused;
+  constexpr bool kHalf = kGen && MODE == kModeFused && (VAR & kVarHalf);  // half-lane 64 KB block
+  constexpr bool kSplit = MODE == kModeFused && !kHalf;
+  constexpr int kH2 = kHalf ? 2 : 1;
   constexpr bool kTable = MODE != kModeDs;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = smem_addr(smem);
-  Layout L = kSplit ? make_layout_split(base, p.smem_bytes, p.slot)
-                    : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
+  Layout L = kSplit  ? make_layout_split(base, p.smem_bytes, p.slot)
+             : kHalf ? make_layout_half(base, p.smem_bytes, p.slot)
+                     : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
                                   MODE == kModeRaw ? kRemapBytes : 0u);
   if (p.max_stages > 0 && L.stages > p.max_stages) {
     L.stages = p.max_stages;
@@ -497,7 +527,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // at out_off, the image of that tile's output bytes at the destination's alignment mod 16;
   // the producer writes its 16-byte-aligned interior with one bulk store, the consumers write
   // the < 16-byte head and tail fragments (shared with the neighbouring tiles) directly.
-  const bool kStaged = kGen && p.out_off != 0u;
+  // (downsample-only kernel only: the fused one keeps direct stores and none of this code)
+  constexpr bool kCanStage = kGen && MODE == kModeDs;
+  const bool kStaged = kCanStage && p.out_off != 0u;
   const int64_t ow3 = (int64_t)(p.width / 2) * 3;
 
   if (warp == kConsWarps) {
@@ -603,7 +635,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   // ---------------- consumers ----------------
   const int ctid = threadIdx.x;  // 0 .. kConsThreads-1
   // split layout: channels 0/1 in the 64 KB block after tab2, channel 2 in tab2 (half lanes)
-  const uint32_t lane4 = (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
+  const uint32_t lane4 = kHalf ? L.table | ((uint32_t)lane >> 1 << 2)
+                              : (kSplit ? L.table + kTab2Bytes : L.table) | ((uint32_t)lane << 2);
   const uint32_t lane4h = L.table | ((uint32_t)lane >> 1 << 2);
   int s = 0;
   uint32_t ph = 0;
@@ -682,7 +715,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
         const uint32_t c = (uint32_t)r >> 8, key = (uint32_t)r & 255u;
         uint32_t sum = 0;
-        if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
+        if (kHalf) {  // tab[key][c]: 64-byte half-lane rows in 256-byte key rows
+          const uint32_t ra = L.table + key * 256u + c * 64u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 v = lds128(ra + (uint32_t)(((j + r) & 3) * 16));
+            sum += v.x + v.y + v.z + v.w;
+          }
+        } else if (kSplit && c == 2) {  // tab2[key]: 64-byte rows
           const uint32_t ra = L.table + key * 64u;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -810,8 +850,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit_any(a, wt);
           load_unit_any(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<true>(wt, lane4, lane4h);
-            hist_unit_pair<true>(wb, lane4, lane4h);
+            hist_unit_pair<kH2>(wt, lane4, lane4h);
+            hist_unit_pair<kH2>(wb, lane4, lane4h);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -839,8 +879,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             load_unit_any(a, wt);
             load_unit_any(a + rg.rowb, wb);
             if constexpr (MODE == kModeFused) {
-              hist_unit_pair<true>(wt, lane4, lane4h);
-              hist_unit_pair<true>(wb, lane4, lane4h);
+              hist_unit_pair<kH2>(wt, lane4, lane4h);
+              hist_unit_pair<kH2>(wb, lane4, lane4h);
             }
             if (dsf) ds_unit(wt, wb, o);
           }
@@ -864,8 +904,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit(a, wt);
           load_unit(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<true>(wt, lane4, lane4h);
-            hist_unit_pair<true>(wb, lane4, lane4h);
+            hist_unit_pair<kH2>(wt, lane4, lane4h);
+            hist_unit_pair<kH2>(wb, lane4, lane4h);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -903,7 +943,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           uint32_t w[12];
           if constexpr (kGen) load_unit_any(slot + (rows - 1) * rg.rowb + v * 48u, w);
           else load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
-          hist_unit_pair<true>(w, lane4, lane4h);
+          hist_unit_pair<kH2>(w, lane4, lane4h);
         }
       }
     } else {
@@ -1082,8 +1122,8 @@ struct Knobs {
   uint32_t prod_sleep = 0;    // SCN_PROD_SLEEP: producer empty-slot wait suspend hint in ns (0 = spin)
   int hist_warps = 0;         // SCN_HIST_WARPS: consumer warps of the hist-only kernels (tuning build: 8/20)
   int gen_stage = 1;          // SCN_GEN_STAGE: kVarGen downsample-only output through the staged bulk
-                              // store (0 = the direct cross-lane stores, kept for montage canvases;
-                              // 2 = the fused kernel staged too)
+                              // store (0 = the direct cross-lane stores, kept for montage canvases)
+  int gen_half = 1;           // SCN_GEN_HALF: 0 = never the half-lane fused layout (A/B)
   int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
                               // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
@@ -1108,6 +1148,7 @@ static void read_knobs_once() {
   k.prod_sleep = (uint32_t)env_int("SCN_PROD_SLEEP", 0);
   k.gen_warps = env_int("SCN_GEN_WARPS", 0);
   k.gen_stage = env_int("SCN_GEN_STAGE", 1);
+  k.gen_half = env_int("SCN_GEN_HALF", 1);
   k.hist_warps = env_int("SCN_HIST_WARPS", 0);
   g_knobs = k;
 }
@@ -1206,10 +1247,11 @@ static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile, boo
 // smem base = the per-block reserved size): the largest even row count (tile <= 64 KB)
 // whose slots give >= 3 ring stages over the two ring segments; 0 if none. The device
 // recomputes the same layout and traps on < 2 stages.
-static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged) {
+static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged, bool half = false) {
   const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin;
-  const uint32_t block = (base + kCtrlBytes + kTab2Bytes + 65535u) & ~65535u;
-  const uint32_t tab2 = block - kTab2Bytes, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
+  const uint32_t t2 = half ? 0u : kTab2Bytes;  // make_layout_half: no tab2 below the block
+  const uint32_t block = (base + kCtrlBytes + t2 + 65535u) & ~65535u;
+  const uint32_t tab2 = block - t2, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
   if (hi > end) return 0;
   auto stages = [&](int r) {
     const uint32_t slot = slot_bytes(r, rowb, slack, staged), stride = (slot + 127u) & ~127u;
@@ -1377,8 +1419,24 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   const bool gen = !rowpair_aligned(j.width, pitch, j.ds_out);
   // the realigning fused kernel keeps direct stores: its ring slots are worth more as input
   // (a staged slot would cost two rows per tile; measured slower, DESIGN.md §5 kVarGen)
-  const bool staged = gen && knobs().gen_stage == 2 && staged_ok(j.width, pitch, j.ds_cols);  // tuning A/B only
-  const int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged);
+  const bool staged = false;
+  int rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged);
+  // The realigning kernel pays a per-tile cost (tails, frame bookkeeping, the slot hand-off) that
+  // bigger tiles amortise: where the half-lane 64 KB block admits more rows per tile than the
+  // split 80 KB table AND that tile holds at most one unit pair per thread of 16 consumer
+  // warps (no warp runs a second, mostly idle iteration and holds the slot), take it
+  // (measured same box, profiles/r02_tune_gen2.jsonl: 1366x768 10 -> 12 rows = 510 unit
+  // pairs, +6.6 %; 426x240 36 -> 40 rows = 520 pairs, 16 warps -12 %: kept on the split
+  // table; 854x480 gains no rows: the half-lane block alone costs 1.5 % in bank conflicts)
+  bool half = false;
+  if (gen && knobs().fused_tile == 0 && knobs().gen_half != 0) {
+    const int rh = rows_per_tile_split((int64_t)j.width * 3, kGenSlack, 0, staged, true);
+    const int64_t pairs = (int64_t)(rh / 2) * (j.width / 16);
+    if (rh > rpt && rpt < j.height && pairs <= 32 * kGenHalfWarps) {
+      half = true;
+      rpt = rh;
+    }
+  }
   const bool fused = divides16(j.bins) && hist_impl() == 0 && rpt >= 2 && j.n_halo == 0 && j.width >= 2 &&
                      j.height >= 2;
   if (!fused) {  // two passes: histogram, then downsample
@@ -1394,9 +1452,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   }
   HistParams p = base_params(j);
   rowpair_tiles(p, rpt, gen, staged);
-  p.table_bytes = kTab2Bytes + 65536u;  // tab2 + the channel 0/1 block, zeroed as one range
+  p.table_bytes = half ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
+  if (half) return launch_tma<kModeFused, kGenHalfWarps, kVarGen | kVarHalf>(p, st);
   return gen ? launch_gen<kModeFused>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
 }
 

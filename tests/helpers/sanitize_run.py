@@ -58,6 +58,11 @@ def main():
     check(w4, ("hist", "downsample"), 16)
     check(w4, ("downsample",), 16, fused=False)
     unaligned_out(w4)
+    # the half-lane fused layout (1366 wide: 12-row tiles, 16 warps) and the staged bulk-store
+    # downsample over several tiles with an odd last row
+    w5 = Workload("san5", 1366, 29, 1, 3, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 3})
+    check(w5, ("hist", "downsample"), 16)
+    check(w5, ("downsample",), 16, fused=False)
     # the north_star's K2a and K2a' (per-warp bins, __match_any_sync)
     import paper_1805_07339_b200 as scn
     for impl in (1, 2):
@@ -79,6 +84,17 @@ def joint(wl, j):
     scn.scn_run_histogram_joint(job.seq, 0, M, j, out, job.stream)
     torch.cuda.synchronize()
     assert (out.cpu().numpy().view(np.uint32) == oracle.run_joint(wl.spec(), pl[0], pl[1], 0, M, j)).all()
+    job.close()
+    # joint shot-diff over a shard that needs its [-1,0] halo
+    b = M // 2
+    job = scn_harness.DeviceJob(wl, b, M, with_halo=True, plan_=pl)
+    H = torch.empty((M - b, j ** 3), dtype=torch.int32, device="cuda")
+    D = torch.empty(M - b, dtype=torch.int32, device="cuda")
+    scratch = torch.empty(j ** 3, dtype=torch.int32, device="cuda")
+    scn.scn_run_hist_shotdiff_joint(job.seq, b, M, j, H, D, scratch, job.stream)
+    torch.cuda.synchronize()
+    rh, rd = oracle.run_joint_diff(wl.spec(), pl[0], pl[1], pl[2], b, M, j)
+    assert (H.cpu().numpy().view(np.uint32) == rh).all() and (D.cpu().numpy().view(np.uint32) == rd).all()
     job.close()
 
 

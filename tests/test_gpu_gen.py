@@ -24,8 +24,9 @@ def _job(w, h, frames, mode="shots"):
     return wl, job, M, H, DS
 
 
-@pytest.mark.parametrize("w,h", [(1366, 24), (854, 33), (426, 18), (67, 41), (17, 5), (15, 9), (3, 3), (2, 2),
-                                 (1920, 17), (33, 64)])
+# (1366, 37): the half-lane fused layout (12-row tiles, 16 warps) over 4 tiles, the last one odd
+@pytest.mark.parametrize("w,h", [(1366, 24), (1366, 37), (854, 33), (426, 18), (67, 41), (17, 5), (15, 9), (3, 3),
+                                 (2, 2), (1920, 17), (33, 64)])
 @pytest.mark.parametrize("offset", [0, 1, 2, 4, 5])
 def test_unaligned_widths_and_outputs(w, h, offset):
     wl, job, M, H, DS = _job(w, h, 7)
