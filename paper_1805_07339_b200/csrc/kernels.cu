@@ -30,9 +30,12 @@
 // K4     MODE kDs     the same row-pair ring without the table (downsample only).
 //   VAR kVarGen (both row-pair modes): any width and any output alignment — rows are
 //   re-aligned in registers after the bulk copy (4 x LDS.128 + 12 funnel shifts per
-//   unit), the W mod 16 tail pixels of each row take a bytewise path, and unaligned
-//   output rows are written as aligned 8-byte words assembled across neighbouring
-//   lanes with one shuffle pair.
+//   unit), the W mod 16 tail pixels of each row take a bytewise path. Output: the
+//   downsample-only kernel stages each tile's output rows in its ring slot and the
+//   producer writes them with one TMA bulk store (cp.async.bulk.global.shared::cta);
+//   the fused kernel (and montage canvases) write aligned 8-byte words assembled across
+//   neighbouring lanes with one shuffle pair. VAR kVarHalf (fused, where it buys a bigger
+//   tile): a half-lane 64 KB key block, every key one PRMT.
 // K2a    MODE kMatch  the north_star's design, selectable (scn_set_hist_impl): per-warp
 //   bins, __match_any_sync peer groups per byte, leader atomicAdd(popc), __reduce_add_sync
 //   merge across warps, one global add per key per block.
@@ -40,8 +43,8 @@
 //   pair keys (8 bytes), so MATCH issues 1/8 as often; per-warp pair-key bins.
 // K2j    MODE kJoint (NEXT N4's joint-colour variant): one key per pixel,
 //   k = bin(R)*J*J + bin(G)*J + bin(B), J <= 8, into J^3 lane-private 128-byte rows; for J = 2^L
-//   each channel's bin field is cut with one SHF and OR-ed into the row address with one LOP3.
-// K3     shotdiff_kernel: one warp per position, L1 over 3*B counters, __reduce_add_sync.
+//   four bytes are binned per two 16-bit-lane IMADs and a pixel keyed with one IDP.4A.
+// K3     shotdiff_kernel: one warp per position, L1 over 3*B (or J^3) counters, __reduce_add_sync.
 //
 // Why not the north_star's per-warp bins + __match_any_sync aggregation as the default:
 // on this B200 MATCH.ANY issues at 0.035 warp-instr/clk/SM (profiles/r01_k0_micro_v2.json),
@@ -296,48 +299,40 @@ __device__ __forceinline__ void match_packed_word(const uint32_t* w, uint32_t am
 }
 
 // ---- NEXT N4 joint-colour keys: one key per pixel, k = (bR * J + bG) * J + bB ------------
-// Pixel P of a unit is bytes 3P..3P+2; each channel byte is zero-extended by one PRMT and
-// binned as (v * J) >> 8 (reading Q2); the key picks a 128-byte lane-private row.
+// Pixel P of a unit is bytes 3P..3P+2 (reading Q2 bins, (v * J) >> 8); the key picks a 128-byte
+// lane-private row.
+// Any J, SIMD: the bins of a word's four bytes come from two 16-bit-lane products,
+// (v * J) >> 8 for bytes 0/2 and 1/3 at once (v * J < 2^16), i.e. 2 PRMT + 2 IMAD + SHF + LOP3
+// per 4 bytes; a pixel's key bin(R)*J^2 + bin(G)*J + bin(B) is then ONE IDP.4A of its 4-byte
+// window of bins (a funnel shift for 12 of the 16 pixels) against (J^2, J, 1, 0), and its row
+// address one LEA: ~2.75 instructions per byte. Measured (profiles/r02_tune_joint.jsonl, same
+// box): every J at 7.24-7.33 TB/s; a multiply per channel byte ran J = 3/5/7 at 5.5 TB/s, and
+// the shift-and-OR bin fields for J = 2^L (3 SHF + 3 LOP3 per pixel) 6.4-6.9 TB/s.
+__device__ __forceinline__ uint32_t joint_bins4(uint32_t w, uint32_t J) {
+  const uint32_t lo = __byte_perm(w, 0u, 0x4240u) * J;  // [0, b2, 0, b0] * J
+  const uint32_t hi = __byte_perm(w, 0u, 0x4341u) * J;  // [0, b3, 0, b1] * J
+  uint32_t B;  // (lo >> 8) & 0x00FF00FF | hi & 0xFF00FF00: one LOP3 (LUT 0xCA = M ? a : b per bit)
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(B) : "r"(0x00FF00FFu), "r"(lo >> 8), "r"(hi));
+  return B;
+}
 template <int P>
-__device__ __forceinline__ uint32_t joint_key(const uint32_t* w, uint32_t J) {
-  constexpr int i0 = 3 * P, i1 = 3 * P + 1, i2 = 3 * P + 2;
-  const uint32_t r = __byte_perm(w[i0 >> 2], 0u, 0x4440u + (i0 & 3));
-  const uint32_t g = __byte_perm(w[i1 >> 2], 0u, 0x4440u + (i1 & 3));
-  const uint32_t b = __byte_perm(w[i2 >> 2], 0u, 0x4440u + (i2 & 3));
-  return (((r * J) >> 8) * J + ((g * J) >> 8)) * J + ((b * J) >> 8);
+__device__ __forceinline__ void joint_simd_step(const uint32_t* b, uint32_t lane4, uint32_t wts) {
+  constexpr int i = 3 * P;
+  const uint32_t win = (i & 3) ? __funnelshift_r(b[i >> 2], b[(i >> 2) + 1], 8 * (i & 3)) : b[i >> 2];
+  red_shared_add_off<0>(lane4 + (__dp4a(win, wts, 0u) << 7));
 }
 template <int... P>
-__device__ __forceinline__ void joint_unit_all(const uint32_t* w, uint32_t lane4, uint32_t J,
+__device__ __forceinline__ void joint_simd_all(const uint32_t* b, uint32_t lane4, uint32_t wts,
                                                std::integer_sequence<int, P...>) {
-  (red_shared_add_off<0>(lane4 + joint_key<P>(w, J) * 128u), ...);
+  (joint_simd_step<P>(b, lane4, wts), ...);
 }
 __device__ __forceinline__ void hist_unit_joint(const uint32_t* w, uint32_t lane4, uint32_t J) {
-  joint_unit_all(w, lane4, J, std::make_integer_sequence<int, 16>{});
+  uint32_t b[13];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) b[k] = joint_bins4(w[k], J);
+  b[12] = 0u;  // pixel 15's window reads bytes 45..48: byte 48 has weight 0
+  joint_simd_all(b, lane4, J * J | J << 8 | 1u << 16, std::make_integer_sequence<int, 16>{});
 }
-// J = 2^L: bin(v) = v >> (8 - L), so each channel's bin field is cut from its word by one shift
-// and OR-ed into the row address (table | k << 7 | lane << 2) by one LOP3 with a constant mask:
-// 3 SHF + 3 LOP3 + 1 ATOMS per pixel (the generic path needs 12 ALU/FMA ops per pixel).
-template <int L, int I, int T>
-__device__ __forceinline__ uint32_t joint_field(const uint32_t* w, uint32_t acc) {
-  constexpr int s = 8 * (I & 3) + 8 - L - T;  // bring the byte's top L bits to bit T
-  const uint32_t x = s >= 0 ? (w[I >> 2] >> (s >= 0 ? s : 0)) : (w[I >> 2] << (s < 0 ? -s : 0));
-  return lop3_and_or<((1u << L) - 1u) << T>(x, acc);
-}
-template <int L, int P>
-__device__ __forceinline__ void joint_pow2_step(const uint32_t* w, uint32_t lane4) {
-  uint32_t a = joint_field<L, 3 * P + 2, 7>(w, lane4);      // B: bits 7 ..
-  a = joint_field<L, 3 * P + 1, L + 7>(w, a);               // G
-  red_shared_add_off<0>(joint_field<L, 3 * P, 2 * L + 7>(w, a));  // R
-}
-template <int L, int... P>
-__device__ __forceinline__ void joint_pow2_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, P...>) {
-  (joint_pow2_step<L, P>(w, lane4), ...);
-}
-template <int L>
-__device__ __forceinline__ void hist_unit_joint_pow2(const uint32_t* w, uint32_t lane4) {
-  joint_pow2_all<L>(w, lane4, std::make_integer_sequence<int, 16>{});
-}
-
 __device__ __forceinline__ void load_unit(uint32_t a, uint32_t* w) {  // 48 bytes at a 16-byte aligned address
   const uint4 v0 = lds128(a), v1 = lds128(a + 16), v2 = lds128(a + 32);
   w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
@@ -957,13 +952,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         } else if constexpr (MODE == kModeRaw) {
           hist_unit_raw(w, lane4);
         } else if constexpr (MODE == kModeJoint) {
-          switch (p.joint) {  // uniform over the launch
-            case 1: hist_unit_joint_pow2<0>(w, lane4); break;
-            case 2: hist_unit_joint_pow2<1>(w, lane4); break;
-            case 4: hist_unit_joint_pow2<2>(w, lane4); break;
-            case 8: hist_unit_joint_pow2<3>(w, lane4); break;
-            default: hist_unit_joint(w, lane4, (uint32_t)p.joint);
-          }
+          hist_unit_joint(w, lane4, (uint32_t)p.joint);
         } else if constexpr (MODE == kModeMatch) {
           // north_star K2a: per-warp bins, peers found with __match_any_sync, one leader
           // atomic of popc(peers) per peer group
@@ -1358,8 +1347,7 @@ cudaError_t launch_histogram_joint(const HistJob& j, cudaStream_t st, int* launc
   p.total_tiles = p.n_items * p.tpf;
   p.l2_prefetch = knobs().l2_prefetch_hist;
   p.table_bytes = (uint32_t)(j.joint * j.joint * j.joint) * 128u;
-  // J = 2^L ORs the bin fields into the table address: align the table to its own size
-  p.table_align = (j.joint & (j.joint - 1)) == 0 ? p.table_bytes : 128u;
+  p.table_align = 128u;  // row address = table + key * 128 + lane * 4 (LEA), any alignment
   *launches += 1;
   return launch_tma<kModeJoint, kHistWarps>(p, st);
 }
