@@ -40,6 +40,9 @@ run hist_k2ap 512 C2 hist 0 "" 2
 REPS=1 timeout 900 ncu --metrics $M --clock-control none -k regex:hist_tma_kernel -s 3 -c 1 --csv \
   --log-file $O/counters_hist_joint8.csv python bench.py --joint 8 --frames 2048 --steps 1 --warmup 3 > $O/counters_hist_joint8.log 2>&1
 python tools/ncu_summarize.py $O/counters_hist_joint8.csv hist_joint8 2048 C2 hist 0 "" $SHA > $O/counters_hist_joint8.json
+REPS=1 timeout 900 ncu --metrics $M --clock-control none -k regex:hist_tma_kernel -s 3 -c 1 --csv \
+  --log-file $O/counters_hist_joint3.csv python bench.py --joint 3 --frames 2048 --steps 1 --warmup 3 > $O/counters_hist_joint3.log 2>&1
+python tools/ncu_summarize.py $O/counters_hist_joint3.csv hist_joint3 2048 C2 hist 0 "" $SHA > $O/counters_hist_joint3.json
 # full-set captures of the two headline kernels -> traffic summaries (bytes per frame, SHA)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:hist_tma_kernel -s 3 -c 1 -o $O/full_hist \
   python tools/hist_tune.py shots 2048 C2 hist --reps 1 > $O/full_hist.log 2>&1; echo "full hist $?"
