@@ -62,7 +62,8 @@
 namespace scn {
 
 enum : int {
-  kModePair = 0, kModeFused = 2, kModeDs = 3, kModeRaw = 4, kModeMatch = 5, kModeMatchPacked = 6, kModeJoint = 7
+  kModePair = 0, kModeFused = 2, kModeDs = 3, kModeRaw = 4, kModeMatch = 5, kModeMatchPacked = 6, kModeJoint = 7,
+  kModePairB = 8
 };
 constexpr int kVarGen = 1;   // row-pair modes: any width / output alignment
 constexpr int kVarHalf = 2;  // fused kVarGen: half-lane 64 KB key block (see pair_key_step)
@@ -326,6 +327,25 @@ __device__ __forceinline__ void joint_simd_all(const uint32_t* b, uint32_t lane4
                                                std::integer_sequence<int, P...>) {
   (joint_simd_step<P>(b, lane4, wts), ...);
 }
+// ---- K2b: any B <= 16 as pair keys of SIMD bins ---------------------------------------------
+// The bins of bytes j and j+24 (same channel) of a unit, from joint_bins4 (B <= 16: bins < 16),
+// form the key word bins(w[k]) | bins(w[k+6]) << 4 (one IMAD: no carries), i.e. the K1 pair
+// keys with B-level instead of 16-level fields: 0.5 shared atomics per byte for every B <= 16
+// (K2r, one atomic per byte, keeps B > 16). The flush adds each key to both of its bins.
+__device__ __forceinline__ uint32_t joint_bins4(uint32_t w, uint32_t J);
+template <int K_>
+__device__ __forceinline__ void pair_word_bins(const uint32_t* w, uint32_t lane4, uint32_t B) {
+  const uint32_t Kw = joint_bins4(w[K_ + 6], B) * 16u + joint_bins4(w[K_], B);
+  pair_key_step<K_, 0, false>(Kw, lane4, 0u);
+  pair_key_step<K_, 1, false>(Kw, lane4, 0u);
+  pair_key_step<K_, 2, false>(Kw, lane4, 0u);
+  pair_key_step<K_, 3, false>(Kw, lane4, 0u);
+}
+__device__ __forceinline__ void hist_unit_pair_bins(const uint32_t* w, uint32_t lane4, uint32_t B) {
+  pair_word_bins<0>(w, lane4, B); pair_word_bins<1>(w, lane4, B); pair_word_bins<2>(w, lane4, B);
+  pair_word_bins<3>(w, lane4, B); pair_word_bins<4>(w, lane4, B); pair_word_bins<5>(w, lane4, B);
+}
+
 __device__ __forceinline__ void hist_unit_joint(const uint32_t* w, uint32_t lane4, uint32_t J) {
   uint32_t b[13];
 #pragma unroll
@@ -757,7 +777,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
       }
     } else if (MODE != kModeJoint && ctid < 3 * B) {  // B divides 16: bin b of channel c merges 16/B adjacent 16-level bins
-      const int c = ctid / B, b = ctid - c * B, g = 16 / B;
+      const int c = ctid / B, b = ctid - c * B, g = MODE == kModePairB ? 1 : 16 / B;
       uint32_t v = 0;
       for (int k = 0; k < g; ++k) {
         v += hsum[c * 16 + b * g + k];
@@ -949,6 +969,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         load_unit(slot + u * 48u, w);
         if constexpr (MODE == kModePair) {
           hist_unit_pair<false>(w, lane4);
+        } else if constexpr (MODE == kModePairB) {
+          hist_unit_pair_bins(w, lane4, (uint32_t)B);
         } else if constexpr (MODE == kModeRaw) {
           hist_unit_raw(w, lane4);
         } else if constexpr (MODE == kModeJoint) {
@@ -1113,6 +1135,7 @@ struct Knobs {
   int gen_stage = 1;          // SCN_GEN_STAGE: kVarGen downsample-only output through the staged bulk
                               // store (0 = the direct cross-lane stores, kept for montage canvases)
   int gen_half = 1;           // SCN_GEN_HALF: 0 = never the half-lane fused layout (A/B)
+  int pair_bins = 1;          // SCN_PAIR_BINS: 0 = bins < 16 not dividing 16 on K2r instead of K2b (A/B)
   int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
                               // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
@@ -1138,6 +1161,7 @@ static void read_knobs_once() {
   k.gen_warps = env_int("SCN_GEN_WARPS", 0);
   k.gen_stage = env_int("SCN_GEN_STAGE", 1);
   k.gen_half = env_int("SCN_GEN_HALF", 1);
+  k.pair_bins = env_int("SCN_PAIR_BINS", 1);
   k.hist_warps = env_int("SCN_HIST_WARPS", 0);
   g_knobs = k;
 }
@@ -1163,6 +1187,7 @@ const char* hist_variant_name(int32_t bins) {
       default: return "tma_pair_lane_private";
     }
   }
+  if (bins < 16 && knobs().pair_bins != 0) return "tma_pair_bins_lane_private";
   return "tma_raw_lane_private_remap";
 }
 
@@ -1327,6 +1352,7 @@ cudaError_t launch_histogram(const HistJob& j, cudaStream_t st, int* launches) {
   }
   p.table_bytes = 3u * 256u * 128u;
   p.table_align = 65536u;
+  if (j.bins < 16 && knobs().pair_bins != 0) return launch_tma<kModePairB, kHistWarps>(p, st);  // K2b
 #ifdef SCN_TUNING
   if (knobs().hist_warps == 8) return launch_tma<kModeRaw, 8>(p, st);
   if (knobs().hist_warps == 20) return launch_tma<kModeRaw, 20>(p, st);

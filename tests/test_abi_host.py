@@ -360,6 +360,7 @@ def test_adaptive_cuts_overflow_bound_and_hist_impl_validation():
         assert e.value.status == scn.SCN_EINVAL
     assert scn.scn_hist_variant(16) == "tma_pair_lane_private"
     assert scn.scn_hist_variant(100) == "tma_raw_lane_private_remap"
+    assert scn.scn_hist_variant(5) == "tma_pair_bins_lane_private"
     scn.scn_set_hist_impl(scn.SCN_HIST_MATCH_PACKED)
     assert scn.scn_hist_variant(8) == "k2a_packed_match_per_warp"
     assert scn.scn_hist_variant(256) == "tma_raw_lane_private_remap"

@@ -251,11 +251,12 @@ def test_fused_gather_local_destinations():
         scn.scn_run_hist_shotdiff_to(job.seq, 0, 1, 16, [], [], 0, scratch)
 
 
-@pytest.mark.parametrize("bins", [2, 3, 8, 17, 100, 128, 255])
+@pytest.mark.parametrize("bins", [2, 3, 5, 7, 8, 12, 15, 17, 100, 128, 255])
 @pytest.mark.parametrize("mode", ["uniform", "shots"])
 def test_every_bin_kernel_path(bins, mode):
-    # bins dividing 16 merge 16-level pair-key bins at the flush; every other B counts raw values
-    # and maps them to bins at the flush (K2r) — uniform content reaches every bin edge
+    # bins dividing 16 merge 16-level pair-key bins at the flush; other B < 16 pair SIMD-computed
+    # bins (K2b); B > 16 counts raw values and maps them to bins at the flush (K2r) — uniform
+    # content reaches every bin edge
     wl = Workload("bins", 211, 37, 2, 12, ("stride", 1), ("hist", "shotdiff"), bins=bins,
                   spec_kw={"len_min": 2, "len_max": 5})
     v, r, s = _oracle_positions(wl)
@@ -264,4 +265,5 @@ def test_every_bin_kernel_path(bins, mode):
     got = _run(wl, 0, len(r), ("hist", "shotdiff"), bins, spec=spec)
     np.testing.assert_array_equal(got["hist"], H)
     np.testing.assert_array_equal(got["diff"], D)
-    assert scn.scn_hist_variant(bins) == ("tma_pair_lane_private" if 16 % bins == 0 else "tma_raw_lane_private_remap")
+    assert scn.scn_hist_variant(bins) == ("tma_pair_lane_private" if 16 % bins == 0 else
+                                          "tma_pair_bins_lane_private" if bins < 16 else "tma_raw_lane_private_remap")
