@@ -6,6 +6,8 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 # the library's version = the last commit that changed its sources (doc-only commits keep it,
 # so ncu captures of the same kernels stay matched to the library, bench.py traffic_source)
 GIT_SHA   := $(shell git log -1 --format=%h --abbrev=12 -- paper_1805_07339_b200/csrc include Makefile 2>/dev/null | grep . || echo unknown)
+# uncommitted changes to those sources mark the build (a capture of it matches no commit)
+GIT_SHA   := $(GIT_SHA)$(shell git status --porcelain -- paper_1805_07339_b200/csrc include Makefile 2>/dev/null | grep -q . && echo -dirty)
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -shared -cudart static
 CC        ?= gcc
 CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra -shared
