@@ -10,6 +10,8 @@ if [ "${1:-}" != "notest" ]; then
   tail -3 $O/pytest_gpu.log
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 fi
+# traffic summaries of THIS library first, so every bench line's roofline.traffic_source matches it
+bash tools/gpu_r02_traffic.sh > $O/traffic_pass.log 2>&1; cp gpurun_out/r02/traffic/ncu_*_summary.json profiles/; echo "traffic $?"
 B="timeout 900 python bench.py"
 $B > $O/bench_C2.json 2> $O/bench_C2.err; echo "C2 $?"
 $B --frames 2048 --no-cpu-baseline --no-e2e > $O/bench_C2_2048f_shard_proxy.json 2>/dev/null; echo "proxy $?"
