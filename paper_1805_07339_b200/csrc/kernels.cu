@@ -67,6 +67,7 @@ enum : int {
 };
 constexpr int kVarGen = 1;   // row-pair modes: any width / output alignment
 constexpr int kVarHalf = 2;  // fused kVarGen: half-lane 64 KB key block (see pair_key_step)
+constexpr int kVarBins = 4;  // fused: pair keys of B-level bins (B < 16 not dividing 16, see K2b)
 
 constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 producer warp)
 constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only kernels
@@ -333,17 +334,26 @@ __device__ __forceinline__ void joint_simd_all(const uint32_t* b, uint32_t lane4
 // keys with B-level instead of 16-level fields: 0.5 shared atomics per byte for every B <= 16
 // (K2r, one atomic per byte, keeps B > 16). The flush adds each key to both of its bins.
 __device__ __forceinline__ uint32_t joint_bins4(uint32_t w, uint32_t J);
-template <int K_>
-__device__ __forceinline__ void pair_word_bins(const uint32_t* w, uint32_t lane4, uint32_t B) {
+template <int K_, int H2>
+__device__ __forceinline__ void pair_word_bins(const uint32_t* w, uint32_t lane4, uint32_t lane4h, uint32_t B) {
   const uint32_t Kw = joint_bins4(w[K_ + 6], B) * 16u + joint_bins4(w[K_], B);
-  pair_key_step<K_, 0, false>(Kw, lane4, 0u);
-  pair_key_step<K_, 1, false>(Kw, lane4, 0u);
-  pair_key_step<K_, 2, false>(Kw, lane4, 0u);
-  pair_key_step<K_, 3, false>(Kw, lane4, 0u);
+  pair_key_step<K_, 0, H2>(Kw, lane4, lane4h);
+  pair_key_step<K_, 1, H2>(Kw, lane4, lane4h);
+  pair_key_step<K_, 2, H2>(Kw, lane4, lane4h);
+  pair_key_step<K_, 3, H2>(Kw, lane4, lane4h);
 }
-__device__ __forceinline__ void hist_unit_pair_bins(const uint32_t* w, uint32_t lane4, uint32_t B) {
-  pair_word_bins<0>(w, lane4, B); pair_word_bins<1>(w, lane4, B); pair_word_bins<2>(w, lane4, B);
-  pair_word_bins<3>(w, lane4, B); pair_word_bins<4>(w, lane4, B); pair_word_bins<5>(w, lane4, B);
+template <int H2>
+__device__ __forceinline__ void hist_unit_pair_bins(const uint32_t* w, uint32_t lane4, uint32_t lane4h, uint32_t B) {
+  pair_word_bins<0, H2>(w, lane4, lane4h, B); pair_word_bins<1, H2>(w, lane4, lane4h, B);
+  pair_word_bins<2, H2>(w, lane4, lane4h, B); pair_word_bins<3, H2>(w, lane4, lane4h, B);
+  pair_word_bins<4, H2>(w, lane4, lane4h, B); pair_word_bins<5, H2>(w, lane4, lane4h, B);
+}
+// the fused kernels' histogram of one 48-byte unit: 16-level pair keys, or (kVarBins) pair keys
+// of B-level bins for B < 16 not dividing 16
+template <int H2, bool BINS>
+__device__ __forceinline__ void hist_unit_fused(const uint32_t* w, uint32_t lane4, uint32_t lane4h, uint32_t B) {
+  if constexpr (BINS) hist_unit_pair_bins<H2>(w, lane4, lane4h, B);
+  else hist_unit_pair<H2>(w, lane4, lane4h);
 }
 
 __device__ __forceinline__ void hist_unit_joint(const uint32_t* w, uint32_t lane4, uint32_t J) {
@@ -500,6 +510,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr bool kRowPair = MODE == kModeFused || MODE == kModeDs;
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
   constexpr bool kHalf = kGen && MODE == kModeFused && (VAR & kVarHalf);  // half-lane 64 KB block
+  constexpr bool kBins = MODE == kModePairB || (MODE == kModeFused && (VAR & kVarBins));  // B-level pair keys
   constexpr bool kSplit = MODE == kModeFused && !kHalf;
   constexpr int kH2 = kHalf ? 2 : 1;
   constexpr bool kTable = MODE != kModeDs;
@@ -777,7 +788,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         }
       }
     } else if (MODE != kModeJoint && ctid < 3 * B) {  // B divides 16: bin b of channel c merges 16/B adjacent 16-level bins
-      const int c = ctid / B, b = ctid - c * B, g = MODE == kModePairB ? 1 : 16 / B;
+      const int c = ctid / B, b = ctid - c * B, g = kBins ? 1 : 16 / B;
       uint32_t v = 0;
       for (int k = 0; k < g; ++k) {
         v += hsum[c * 16 + b * g + k];
@@ -865,8 +876,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit_any(a, wt);
           load_unit_any(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<kH2>(wt, lane4, lane4h);
-            hist_unit_pair<kH2>(wb, lane4, lane4h);
+            hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -894,8 +905,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             load_unit_any(a, wt);
             load_unit_any(a + rg.rowb, wb);
             if constexpr (MODE == kModeFused) {
-              hist_unit_pair<kH2>(wt, lane4, lane4h);
-              hist_unit_pair<kH2>(wb, lane4, lane4h);
+              hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
+              hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
             }
             if (dsf) ds_unit(wt, wb, o);
           }
@@ -919,8 +930,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit(a, wt);
           load_unit(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_pair<kH2>(wt, lane4, lane4h);
-            hist_unit_pair<kH2>(wb, lane4, lane4h);
+            hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -940,7 +951,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           if constexpr (MODE == kModeFused) {  // histogram of every tail byte, all rows of the tile
             for (uint32_t r = rg.hq, j = rg.hr; r < rows; r += rg.hdq, j += rg.hdr, (j >= rg.tin) ? (j -= rg.tin, ++r) : 0) {
               const uint32_t v = lds_u8(slot + r * rg.rowb + 48u * rg.upr + j);
-              atomicAdd(&hsum[(j % 3u) * 16u + (v >> 4)], 1u);
+              atomicAdd(&hsum[(j % 3u) * 16u + (kBins ? (v * (uint32_t)B) >> 8 : v >> 4)], 1u);
             }
           }
           if (dsf && rg.tob) {
@@ -958,7 +969,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           uint32_t w[12];
           if constexpr (kGen) load_unit_any(slot + (rows - 1) * rg.rowb + v * 48u, w);
           else load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
-          hist_unit_pair<kH2>(w, lane4, lane4h);
+          hist_unit_fused<kH2, kBins>(w, lane4, lane4h, (uint32_t)B);
         }
       }
     } else {
@@ -970,7 +981,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         if constexpr (MODE == kModePair) {
           hist_unit_pair<false>(w, lane4);
         } else if constexpr (MODE == kModePairB) {
-          hist_unit_pair_bins(w, lane4, (uint32_t)B);
+          hist_unit_pair_bins<0>(w, lane4, 0u, (uint32_t)B);
         } else if constexpr (MODE == kModeRaw) {
           hist_unit_raw(w, lane4);
         } else if constexpr (MODE == kModeJoint) {
@@ -1451,8 +1462,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       rpt = rh;
     }
   }
-  const bool fused = divides16(j.bins) && hist_impl() == 0 && rpt >= 2 && j.n_halo == 0 && j.width >= 2 &&
-                     j.height >= 2;
+  // B < 16 not dividing 16 fuse too, with K2b's pair keys of B-level bins (kVarBins)
+  const bool bins = !divides16(j.bins) && j.bins < 16 && knobs().pair_bins != 0;
+  const bool fused = ((divides16(j.bins) && hist_impl() == 0) || bins) && rpt >= 2 && j.n_halo == 0 &&
+                     j.width >= 2 && j.height >= 2;
   if (!fused) {  // two passes: histogram, then downsample
     HistJob h = j;
     h.ds_out = nullptr;
@@ -1469,6 +1482,11 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   p.table_bytes = half ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
+  if (bins) {
+    if (half) return launch_tma<kModeFused, kGenHalfWarps, kVarGen | kVarHalf | kVarBins>(p, st);
+    return gen ? launch_tma<kModeFused, kGenFusedWarps, kVarGen | kVarBins>(p, st)
+               : launch_tma<kModeFused, kDsWarps, kVarBins>(p, st);
+  }
   if (half) return launch_tma<kModeFused, kGenHalfWarps, kVarGen | kVarHalf>(p, st);
   return gen ? launch_gen<kModeFused>(p, st) : launch_tma<kModeFused, kDsWarps>(p, st);
 }

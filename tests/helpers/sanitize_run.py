@@ -63,6 +63,10 @@ def main():
     w5 = Workload("san5", 1366, 29, 1, 3, ("stride", 1), (), spec_kw={"len_min": 2, "len_max": 3})
     check(w5, ("hist", "downsample"), 16)
     check(w5, ("downsample",), 16, fused=False)
+    # fused hist + downsample at B < 16 not dividing 16 (K2b bins): aligned, realigning, half-lane
+    check(w1, ("hist", "downsample"), 5)
+    check(w4, ("hist", "downsample"), 12)
+    check(w5, ("hist", "downsample"), 3)
     # the north_star's K2a and K2a' (per-warp bins, __match_any_sync)
     import paper_1805_07339_b200 as scn
     for impl in (1, 2):
