@@ -68,6 +68,7 @@ enum : int {
 constexpr int kVarGen = 1;   // row-pair modes: any width / output alignment
 constexpr int kVarHalf = 2;  // fused kVarGen: half-lane 64 KB key block (see pair_key_step)
 constexpr int kVarBins = 4;  // fused: pair keys of B-level bins (B < 16 not dividing 16, see K2b)
+constexpr int kVarRaw = 8;   // fused: raw byte keys in the half-lane block (B > 16, see K2r)
 
 constexpr int kHistWarps = 16;  // consumer warps of the hist-only kernels (+1 producer warp)
 constexpr int kDsWarps = 8;     // consumer warps of the fused / downsample-only kernels
@@ -348,11 +349,23 @@ __device__ __forceinline__ void hist_unit_pair_bins(const uint32_t* w, uint32_t 
   pair_word_bins<2, H2>(w, lane4, lane4h, B); pair_word_bins<3, H2>(w, lane4, lane4h, B);
   pair_word_bins<4, H2>(w, lane4, lane4h, B); pair_word_bins<5, H2>(w, lane4, lane4h, B);
 }
-// the fused kernels' histogram of one 48-byte unit: 16-level pair keys, or (kVarBins) pair keys
-// of B-level bins for B < 16 not dividing 16
-template <int H2, bool BINS>
+// kVarRaw: one raw byte key per byte in the half-lane 64 KB block tab[v][c][lane / 2] (one PRMT:
+// byte -> address byte 1; c * 64 the ATOMS immediate), K2r's keys in 64 KB instead of 96 KB so
+// a fused ring still fits; the flush maps value rows to bins as K2r does.
+template <int J>
+__device__ __forceinline__ void raw_half_step(const uint32_t* w, uint32_t lane4) {
+  red_shared_add_off<(J % 3) * 64>(__byte_perm(w[J >> 2], lane4, 0x7604u | ((J & 3) << 4)));
+}
+template <int... J>
+__device__ __forceinline__ void raw_half_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, J...>) {
+  (raw_half_step<J>(w, lane4), ...);
+}
+// the fused kernels' histogram of one 48-byte unit: 16-level pair keys, (kVarBins) pair keys of
+// B-level bins for B < 16 not dividing 16, or (kVarRaw) raw byte keys for B > 16
+template <int H2, bool BINS, bool RAW>
 __device__ __forceinline__ void hist_unit_fused(const uint32_t* w, uint32_t lane4, uint32_t lane4h, uint32_t B) {
-  if constexpr (BINS) hist_unit_pair_bins<H2>(w, lane4, lane4h, B);
+  if constexpr (RAW) raw_half_all(w, lane4, std::make_integer_sequence<int, 48>{});
+  else if constexpr (BINS) hist_unit_pair_bins<H2>(w, lane4, lane4h, B);
   else hist_unit_pair<H2>(w, lane4, lane4h);
 }
 
@@ -509,7 +522,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr int kThreads = kConsThreads + 32;
   constexpr bool kRowPair = MODE == kModeFused || MODE == kModeDs;
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
-  constexpr bool kHalf = kGen && MODE == kModeFused && (VAR & kVarHalf);  // half-lane 64 KB block
+  constexpr bool kRawF = MODE == kModeFused && (VAR & kVarRaw);  // fused raw byte keys (B > 16)
+  constexpr bool kRawAny = MODE == kModeRaw || kRawF;
+  constexpr bool kHalf = MODE == kModeFused && (VAR & (kVarHalf | kVarRaw));  // half-lane 64 KB block
   constexpr bool kBins = MODE == kModePairB || (MODE == kModeFused && (VAR & kVarBins));  // B-level pair keys
   constexpr bool kSplit = MODE == kModeFused && !kHalf;
   constexpr int kH2 = kHalf ? 2 : 1;
@@ -527,7 +542,13 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);  // 3 x 16 bins (pair modes)
-  uint32_t* remap = reinterpret_cast<uint32_t*>(smem + (L.table + p.table_bytes - base));  // kRaw: 3 x B bins
+  // bin counters of the raw-key modes: kRaw above the table; kRawF in the spare 64-byte quarter
+  // of the half-lane block's 256-byte key rows (counter i at row i / 16, word i % 16)
+  uint32_t* const remap_base = reinterpret_cast<uint32_t*>(smem + (L.table + p.table_bytes - base));
+  auto remap = [&](uint32_t i) -> uint32_t* {
+    if constexpr (kRawF) return reinterpret_cast<uint32_t*>(smem + (L.table - base) + (i >> 4) * 256u + 192u + (i & 15u) * 4u);
+    else return remap_base + i;
+  };
   const int B = p.bins;
   const int RS = MODE == kModeJoint ? p.joint * p.joint * p.joint : 3 * B;  // counters per output row
 
@@ -543,7 +564,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
     for (uint32_t i = threadIdx.x; i < p.table_bytes / 16; i += kThreads) sts128(L.table + 16 * i, make_uint4(0, 0, 0, 0));
     for (int i = threadIdx.x; i < 3 * 16; i += kThreads) hsum[i] = 0;
     if constexpr (MODE == kModeRaw)
-      for (int i = threadIdx.x; i < 3 * 256; i += kThreads) remap[i] = 0;
+      for (int i = threadIdx.x; i < 3 * 256; i += kThreads) *remap((uint32_t)i) = 0;
   }
   __syncthreads();
 
@@ -768,9 +789,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
         sum = total - snap[i];
         snap[i] = total;
         if (sum) {
-          if constexpr (MODE == kModeRaw) {  // value row -> bin (v * B) >> 8
+          if constexpr (kRawAny) {  // value row -> bin (v * B) >> 8
             if (B == 256) emit(item, r, sum);
-            else atomicAdd(&remap[c * B + ((key * (uint32_t)B) >> 8)], sum);
+            else atomicAdd(remap(c * B + ((key * (uint32_t)B) >> 8)), sum);
           } else {  // a pair key counts once in each of its two 16-level bins
             atomicAdd(&hsum[c * 16 + (key >> 4)], sum);
             atomicAdd(&hsum[c * 16 + (key & 15u)], sum);
@@ -779,11 +800,11 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
       }
     }
     named_bar(kBarId, kConsThreads);
-    if constexpr (MODE == kModeRaw) {
+    if constexpr (kRawAny) {
       if (B != 256) {
         for (int i = ctid; i < 3 * B; i += kConsThreads) {
-          const uint32_t v = remap[i];
-          remap[i] = 0;
+          const uint32_t v = *remap((uint32_t)i);
+          *remap((uint32_t)i) = 0;
           if (v) emit(item, i, v);
         }
       }
@@ -876,8 +897,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit_any(a, wt);
           load_unit_any(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
-            hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins, kRawF>(wt, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins, kRawF>(wb, lane4, lane4h, (uint32_t)B);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -905,8 +926,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
             load_unit_any(a, wt);
             load_unit_any(a + rg.rowb, wb);
             if constexpr (MODE == kModeFused) {
-              hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
-              hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
+              hist_unit_fused<kH2, kBins, kRawF>(wt, lane4, lane4h, (uint32_t)B);
+              hist_unit_fused<kH2, kBins, kRawF>(wb, lane4, lane4h, (uint32_t)B);
             }
             if (dsf) ds_unit(wt, wb, o);
           }
@@ -930,8 +951,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           load_unit(a, wt);
           load_unit(a + rg.rowb, wb);
           if constexpr (MODE == kModeFused) {
-            hist_unit_fused<kH2, kBins>(wt, lane4, lane4h, (uint32_t)B);
-            hist_unit_fused<kH2, kBins>(wb, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins, kRawF>(wt, lane4, lane4h, (uint32_t)B);
+            hist_unit_fused<kH2, kBins, kRawF>(wb, lane4, lane4h, (uint32_t)B);
           }
           if (dsf) {
             ds_unit(wt, wb, o);
@@ -951,7 +972,12 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           if constexpr (MODE == kModeFused) {  // histogram of every tail byte, all rows of the tile
             for (uint32_t r = rg.hq, j = rg.hr; r < rows; r += rg.hdq, j += rg.hdr, (j >= rg.tin) ? (j -= rg.tin, ++r) : 0) {
               const uint32_t v = lds_u8(slot + r * rg.rowb + 48u * rg.upr + j);
-              atomicAdd(&hsum[(j % 3u) * 16u + (kBins ? (v * (uint32_t)B) >> 8 : v >> 4)], 1u);
+              if constexpr (kRawF) {
+                if (B == 256) emit(item, (int)((j % 3u) * 256u + v), 1u);
+                else atomicAdd(remap((j % 3u) * (uint32_t)B + ((v * (uint32_t)B) >> 8)), 1u);
+              } else {
+                atomicAdd(&hsum[(j % 3u) * 16u + (kBins ? (v * (uint32_t)B) >> 8 : v >> 4)], 1u);
+              }
             }
           }
           if (dsf && rg.tob) {
@@ -969,7 +995,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
           uint32_t w[12];
           if constexpr (kGen) load_unit_any(slot + (rows - 1) * rg.rowb + v * 48u, w);
           else load_unit(slot + (rows - 1) * rg.rowb + v * 48u, w);
-          hist_unit_fused<kH2, kBins>(w, lane4, lane4h, (uint32_t)B);
+          hist_unit_fused<kH2, kBins, kRawF>(w, lane4, lane4h, (uint32_t)B);
         }
       }
     } else {
@@ -1147,6 +1173,7 @@ struct Knobs {
                               // store (0 = the direct cross-lane stores, kept for montage canvases)
   int gen_half = 1;           // SCN_GEN_HALF: 0 = never the half-lane fused layout (A/B)
   int pair_bins = 1;          // SCN_PAIR_BINS: 0 = bins < 16 not dividing 16 on K2r instead of K2b (A/B)
+  int fused_raw = 1;          // SCN_FUSED_RAW: 0 = B > 16 as K2r histogram + downsample pass (A/B)
   int gen_warps = 0;          // SCN_GEN_WARPS: consumer warps of the kVarGen kernels (tuning build: 8/12/16;
                               // 0 = the defaults kGenDsWarps / kGenFusedWarps)
 };
@@ -1173,6 +1200,7 @@ static void read_knobs_once() {
   k.gen_stage = env_int("SCN_GEN_STAGE", 1);
   k.gen_half = env_int("SCN_GEN_HALF", 1);
   k.pair_bins = env_int("SCN_PAIR_BINS", 1);
+  k.fused_raw = env_int("SCN_FUSED_RAW", 1);
   k.hist_warps = env_int("SCN_HIST_WARPS", 0);
   g_knobs = k;
 }
@@ -1462,9 +1490,19 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       rpt = rh;
     }
   }
-  // B < 16 not dividing 16 fuse too, with K2b's pair keys of B-level bins (kVarBins)
+  // B < 16 not dividing 16 fuse too, with K2b's pair keys of B-level bins (kVarBins). B > 16 fuses
+  // on aligned rows with raw byte keys in the half-lane 64 KB block (kVarRaw; K2r's 96 KB table
+  // leaves no ring): one atomic per byte in 2-way-conflicting half-lane rows makes it the slowest
+  // fused kernel (C4 1080p B = 100: 4.56 TB/s), still 1.2x the two passes (3.80); on realigned
+  // rows it loses to the two passes (1366x768: 3.55 vs 3.80, 16 warps 3.88), so those stay
+  // split (profiles/r02_tune_hist_k2b.jsonl)
   const bool bins = !divides16(j.bins) && j.bins < 16 && knobs().pair_bins != 0;
-  const bool fused = ((divides16(j.bins) && hist_impl() == 0) || bins) && rpt >= 2 && j.n_halo == 0 &&
+  const bool raw = j.bins > 16 && !gen && knobs().fused_raw != 0;
+  if (raw) {
+    rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged, true);
+    half = false;
+  }
+  const bool fused = ((divides16(j.bins) && hist_impl() == 0) || bins || raw) && rpt >= 2 && j.n_halo == 0 &&
                      j.width >= 2 && j.height >= 2;
   if (!fused) {  // two passes: histogram, then downsample
     HistJob h = j;
@@ -1479,9 +1517,10 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   }
   HistParams p = base_params(j);
   rowpair_tiles(p, rpt, gen, staged);
-  p.table_bytes = half ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
+  p.table_bytes = (half || raw) ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
+  if (raw) return launch_tma<kModeFused, kDsWarps, kVarRaw>(p, st);
   if (bins) {
     if (half) return launch_tma<kModeFused, kGenHalfWarps, kVarGen | kVarHalf | kVarBins>(p, st);
     return gen ? launch_tma<kModeFused, kGenFusedWarps, kVarGen | kVarBins>(p, st)

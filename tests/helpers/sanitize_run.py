@@ -67,6 +67,10 @@ def main():
     check(w1, ("hist", "downsample"), 5)
     check(w4, ("hist", "downsample"), 12)
     check(w5, ("hist", "downsample"), 3)
+    # ... and B > 16 (raw byte keys in the half-lane block; B = 256 emits value rows directly)
+    check(w1, ("hist", "downsample"), 100)
+    check(w4, ("hist", "downsample"), 256)
+    check(w5, ("hist", "downsample"), 37)
     # the north_star's K2a and K2a' (per-warp bins, __match_any_sync)
     import paper_1805_07339_b200 as scn
     for impl in (1, 2):
