@@ -349,22 +349,32 @@ __device__ __forceinline__ void hist_unit_pair_bins(const uint32_t* w, uint32_t 
   pair_word_bins<2, H2>(w, lane4, lane4h, B); pair_word_bins<3, H2>(w, lane4, lane4h, B);
   pair_word_bins<4, H2>(w, lane4, lane4h, B); pair_word_bins<5, H2>(w, lane4, lane4h, B);
 }
-// kVarRaw: one raw byte key per byte in the half-lane 64 KB block tab[v][c][lane / 2] (one PRMT:
-// byte -> address byte 1; c * 64 the ATOMS immediate), K2r's keys in 64 KB instead of 96 KB so
-// a fused ring still fits; the flush maps value rows to bins as K2r does.
+// kVarRaw: one raw byte key per byte in the fused kernels' split table (K2r's keys in 80 KB
+// instead of 96 KB so a fused ring still fits): channels 0/1 full-lane in the 64 KB PRMT block
+// (one PRMT: byte -> address byte 1, c * 128 the ATOMS immediate), channel 2 in the half-lane
+// tab2[v][lane / 2] (SHF + LOP3); the flush maps value rows to bins as K2r does.
 template <int J>
-__device__ __forceinline__ void raw_half_step(const uint32_t* w, uint32_t lane4) {
-  red_shared_add_off<(J % 3) * 64>(__byte_perm(w[J >> 2], lane4, 0x7604u | ((J & 3) << 4)));
+__device__ __forceinline__ void raw_split_step(const uint32_t* w, uint32_t lane4, uint32_t lane4h) {
+  constexpr int c = J % 3, sh = 8 * (J & 3);
+  if constexpr (c < 2) {
+    red_shared_add_off<c * 128>(__byte_perm(w[J >> 2], lane4, 0x7604u | ((J & 3) << 4)));
+  } else {  // tab2 | v << 6 | (lane / 2) << 2
+    uint32_t x;
+    if constexpr (sh >= 6) x = w[J >> 2] >> (sh - 6);
+    else x = w[J >> 2] << (6 - sh);
+    red_shared_add_off<0>(lop3_and_or<0xFFu << 6>(x, lane4h));
+  }
 }
 template <int... J>
-__device__ __forceinline__ void raw_half_all(const uint32_t* w, uint32_t lane4, std::integer_sequence<int, J...>) {
-  (raw_half_step<J>(w, lane4), ...);
+__device__ __forceinline__ void raw_split_all(const uint32_t* w, uint32_t lane4, uint32_t lane4h,
+                                              std::integer_sequence<int, J...>) {
+  (raw_split_step<J>(w, lane4, lane4h), ...);
 }
 // the fused kernels' histogram of one 48-byte unit: 16-level pair keys, (kVarBins) pair keys of
 // B-level bins for B < 16 not dividing 16, or (kVarRaw) raw byte keys for B > 16
 template <int H2, bool BINS, bool RAW>
 __device__ __forceinline__ void hist_unit_fused(const uint32_t* w, uint32_t lane4, uint32_t lane4h, uint32_t B) {
-  if constexpr (RAW) raw_half_all(w, lane4, std::make_integer_sequence<int, 48>{});
+  if constexpr (RAW) raw_split_all(w, lane4, lane4h, std::make_integer_sequence<int, 48>{});
   else if constexpr (BINS) hist_unit_pair_bins<H2>(w, lane4, lane4h, B);
   else hist_unit_pair<H2>(w, lane4, lane4h);
 }
@@ -524,14 +534,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   constexpr bool kGen = kRowPair && (VAR & kVarGen);
   constexpr bool kRawF = MODE == kModeFused && (VAR & kVarRaw);  // fused raw byte keys (B > 16)
   constexpr bool kRawAny = MODE == kModeRaw || kRawF;
-  constexpr bool kHalf = MODE == kModeFused && (VAR & (kVarHalf | kVarRaw));  // half-lane 64 KB block
+  constexpr bool kHalf = MODE == kModeFused && (VAR & kVarHalf);  // half-lane 64 KB block
   constexpr bool kBins = MODE == kModePairB || (MODE == kModeFused && (VAR & kVarBins));  // B-level pair keys
   constexpr bool kSplit = MODE == kModeFused && !kHalf;
   constexpr int kH2 = kHalf ? 2 : 1;
   constexpr bool kTable = MODE != kModeDs;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = smem_addr(smem);
-  Layout L = kSplit  ? make_layout_split(base, p.smem_bytes, p.slot)
+  // kRawF keeps its 3 x B bin counters in the top kRemapBytes of shared memory, out of the ring
+  Layout L = kSplit  ? make_layout_split(base, p.smem_bytes - (kRawF ? kRemapBytes : 0u), p.slot)
              : kHalf ? make_layout_half(base, p.smem_bytes, p.slot)
                      : make_layout(base, p.smem_bytes, p.slot, p.table_bytes, p.table_align,
                                   MODE == kModeRaw ? kRemapBytes : 0u);
@@ -542,13 +553,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t full0 = L.ctrl, empty0 = L.ctrl + 8 * kMaxStages;
   uint32_t* hsum = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);  // 3 x 16 bins (pair modes)
-  // bin counters of the raw-key modes: kRaw above the table; kRawF in the spare 64-byte quarter
-  // of the half-lane block's 256-byte key rows (counter i at row i / 16, word i % 16)
-  uint32_t* const remap_base = reinterpret_cast<uint32_t*>(smem + (L.table + p.table_bytes - base));
-  auto remap = [&](uint32_t i) -> uint32_t* {
-    if constexpr (kRawF) return reinterpret_cast<uint32_t*>(smem + (L.table - base) + (i >> 4) * 256u + 192u + (i & 15u) * 4u);
-    else return remap_base + i;
-  };
+  // bin counters of the raw-key modes: kRaw right above the table, kRawF at the top of shared memory
+  uint32_t* const remap_base = kRawF ? reinterpret_cast<uint32_t*>(smem + p.smem_bytes - kRemapBytes)
+                                     : reinterpret_cast<uint32_t*>(smem + (L.table + p.table_bytes - base));
+  auto remap = [&](uint32_t i) -> uint32_t* { return remap_base + i; };
   const int B = p.bins;
   const int RS = MODE == kModeJoint ? p.joint * p.joint * p.joint : 3 * B;  // counters per output row
 
@@ -563,7 +571,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) hist_tma_kernel(const __grid_
   if constexpr (kTable) {  // zero the table and the merge counters
     for (uint32_t i = threadIdx.x; i < p.table_bytes / 16; i += kThreads) sts128(L.table + 16 * i, make_uint4(0, 0, 0, 0));
     for (int i = threadIdx.x; i < 3 * 16; i += kThreads) hsum[i] = 0;
-    if constexpr (MODE == kModeRaw)
+    if constexpr (kRawAny)
       for (int i = threadIdx.x; i < 3 * 256; i += kThreads) *remap((uint32_t)i) = 0;
   }
   __syncthreads();
@@ -1300,8 +1308,9 @@ static int rows_per_tile_ds(int64_t rowb, uint32_t slack, uint32_t env_tile, boo
 // smem base = the per-block reserved size): the largest even row count (tile <= 64 KB)
 // whose slots give >= 3 ring stages over the two ring segments; 0 if none. The device
 // recomputes the same layout and traps on < 2 stages.
-static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged, bool half = false) {
-  const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin;
+static int rows_per_tile_split(int64_t rowb, uint32_t slack, uint32_t env_tile, bool staged, bool half = false,
+                               uint32_t above = 0) {
+  const uint32_t base = (uint32_t)g_smem_reserved, end = base + (uint32_t)g_smem_optin - above;
   const uint32_t t2 = half ? 0u : kTab2Bytes;  // make_layout_half: no tab2 below the block
   const uint32_t block = (base + kCtrlBytes + t2 + 65535u) & ~65535u;
   const uint32_t tab2 = block - t2, ring = (base + kCtrlBytes + 127u) & ~127u, hi = block + 65536u;
@@ -1490,16 +1499,16 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
       rpt = rh;
     }
   }
-  // B < 16 not dividing 16 fuse too, with K2b's pair keys of B-level bins (kVarBins). B > 16 fuses
-  // on aligned rows with raw byte keys in the half-lane 64 KB block (kVarRaw; K2r's 96 KB table
-  // leaves no ring): one atomic per byte in 2-way-conflicting half-lane rows makes it the slowest
-  // fused kernel (C4 1080p B = 100: 4.56 TB/s), still 1.2x the two passes (3.80); on realigned
-  // rows it loses to the two passes (1366x768: 3.55 vs 3.80, 16 warps 3.88), so those stay
-  // split (profiles/r02_tune_hist_k2b.jsonl)
+  // B < 16 not dividing 16 fuse too, with K2b's pair keys of B-level bins (kVarBins); B > 16 with
+  // raw byte keys in the split table (kVarRaw; K2r's 96 KB table leaves no ring), the bin counters
+  // at the top of shared memory. Measured (profiles/r02_tune_hist_k2b.jsonl): C4 1080p B = 100
+  // 5.60 TB/s vs 3.80 for histogram + downsample passes (a half-lane 64 KB block: 4.55),
+  // 1366x768 4.12 vs 3.84, 854x480 3.93 vs 3.59
   const bool bins = !divides16(j.bins) && j.bins < 16 && knobs().pair_bins != 0;
-  const bool raw = j.bins > 16 && !gen && knobs().fused_raw != 0;
-  if (raw) {
-    rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged, true);
+  const bool raw = j.bins > 16 && knobs().fused_raw != 0;
+  if (raw) {  // the split table with the bin counters reserved at the top (kRemapBytes)
+    rpt = rows_per_tile_split((int64_t)j.width * 3, gen ? kGenSlack : 0u, knobs().fused_tile, staged, false,
+                              kRemapBytes);
     half = false;
   }
   const bool fused = ((divides16(j.bins) && hist_impl() == 0) || bins || raw) && rpt >= 2 && j.n_halo == 0 &&
@@ -1517,10 +1526,12 @@ cudaError_t launch_hist_downsample(const HistJob& j, cudaStream_t st, int* launc
   }
   HistParams p = base_params(j);
   rowpair_tiles(p, rpt, gen, staged);
-  p.table_bytes = (half || raw) ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
+  p.table_bytes = half ? 65536u : kTab2Bytes + 65536u;  // (tab2 +) the key block, zeroed as one range
   p.table_align = 65536u;
   *launches += 1;
-  if (raw) return launch_tma<kModeFused, kDsWarps, kVarRaw>(p, st);
+  if (raw)
+    return gen ? launch_tma<kModeFused, kGenFusedWarps, kVarGen | kVarRaw>(p, st)
+               : launch_tma<kModeFused, kDsWarps, kVarRaw>(p, st);
   if (bins) {
     if (half) return launch_tma<kModeFused, kGenHalfWarps, kVarGen | kVarHalf | kVarBins>(p, st);
     return gen ? launch_tma<kModeFused, kGenFusedWarps, kVarGen | kVarBins>(p, st)

@@ -100,9 +100,9 @@ def test_k2a_impls(impl, bins):
         job.close()
 
 
-# Every bin count below 16 runs the FUSED hist + downsample kernels (K2b's pair keys of B-level
-# bins): aligned (W % 16 == 0), realigning and half-lane (1366 wide); B > 16 fuses on aligned rows
-# (raw byte keys in the half-lane block) and takes two passes on realigned rows
+# Every bin count runs the FUSED hist + downsample kernels: B < 16 not dividing 16 with K2b's pair
+# keys of B-level bins (aligned, realigning and half-lane kernels), B > 16 with raw byte keys in the
+# split table (aligned and realigning)
 @pytest.mark.parametrize("bins", [3, 5, 12, 15, 17, 100, 255, 256])
 @pytest.mark.parametrize("w,h", [(64, 36), (640, 49), (1366, 24), (854, 33), (67, 41)])
 def test_fused_any_bins(w, h, bins):
@@ -112,8 +112,7 @@ def test_fused_any_bins(w, h, bins):
     hist = torch.empty((M, 3, bins), dtype=torch.int32, device="cuda")
     ds = torch.empty((M, h // 2, w // 2, 3), dtype=torch.uint8, device="cuda")
     scn.scn_run_hist_downsample(job.seq, 0, M, bins, hist, ds, job.stream)
-    # one fused pass, not histogram + downsample (B > 16 on realigned rows: two passes)
-    assert scn.scn_last_launch_count() == (2 if bins > 16 and w % 16 else 1)
+    assert scn.scn_last_launch_count() == 1  # one fused pass, not histogram + downsample
     torch.cuda.synchronize()
     np.testing.assert_array_equal(hist.cpu().numpy().view(np.uint32), H)
     np.testing.assert_array_equal(ds.cpu().numpy(), DS)
