@@ -29,4 +29,5 @@ run hist_b5_k2b 2048 C2 hist 5 "" 0
 run histds_b5_bins 1024 C4 histds 5 "" 0
 run histds_b100_raw 1024 C4 histds 100 "" 0
 run histds_b5_bins_1366 2048 C4 histds 5 1366x768 0
+run histds_b100_raw_1366 2048 C4 histds 100 1366x768 0
 ls -la $O
