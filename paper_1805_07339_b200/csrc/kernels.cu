@@ -19,11 +19,14 @@
 //   counters with one red.global.add each ("one global merge per block" per frame
 //   segment). B = 1, 2, 4, 8 merge 16/B adjacent 16-level bins at that flush:
 //   bin_B(v) = (v*B) >> 8 = (v >> 4) >> (4 - log2 B) (reading Q2).
-// K2r    MODE kRaw    (every other B in [1,256]): one key per byte, the byte value itself
+// K2b    MODE kPairB  (B < 16 not dividing 16): the K1 pair keys with B-level fields, the bins of
+//   four bytes from two 16-bit-lane IMADs (v*B)>>8: 0.5 shared atomics per byte for every B <= 16.
+// K2r    MODE kRaw    (B in [17,256]): one key per byte, the byte value itself
 //   (256 lane-private rows per channel, PRMT addresses: byte -> address byte 1). The flush
 //   maps value rows to bins, bin = (v*B) >> 8, in shared counters above the table, so any
 //   B runs at the 256-bin kernel's rate (no per-byte multiply).
-// K2f    MODE kFused  (B dividing 16): K1+K2 with the 2x box downsample fused into the
+// K2f    MODE kFused  (any B; VAR kVarBins = K2b keys, kVarRaw = raw keys with the bin counters at
+//   the top of shared memory; default B dividing 16): K1+K2 with the 2x box downsample fused into the
 //   consumer over row-pair tiles (a thread takes two vertically adjacent 48-byte units,
 //   histograms both and emits 8 output pixels with dp4a window sums), so each sampled
 //   frame is read from HBM once (reading Q12). Split table layout: 3 stages of ~46 KB.
@@ -42,8 +45,8 @@
 // K2a'   MODE kMatchPacked  K2a amortised: one __match_any_sync per packed word of four
 //   pair keys (8 bytes), so MATCH issues 1/8 as often; per-warp pair-key bins.
 // K2j    MODE kJoint (NEXT N4's joint-colour variant): one key per pixel,
-//   k = bin(R)*J*J + bin(G)*J + bin(B), J <= 8, into J^3 lane-private 128-byte rows; for J = 2^L
-//   four bytes are binned per two 16-bit-lane IMADs and a pixel keyed with one IDP.4A.
+//   k = bin(R)*J*J + bin(G)*J + bin(B), J <= 8, into J^3 lane-private 128-byte rows; four bytes
+//   are binned per two 16-bit-lane IMADs and a pixel keyed with one IDP.4A.
 // K3     shotdiff_kernel: one warp per position, L1 over 3*B (or J^3) counters, __reduce_add_sync.
 //
 // Why not the north_star's per-warp bins + __match_any_sync aggregation as the default:
