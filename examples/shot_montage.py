@@ -5,6 +5,7 @@ detector (warmup W), then a second job that gathers the first frame of every sho
 tiles their 2x downsamples into a montage, written as a binary PPM.
 
     python examples/shot_montage.py --frames 2000 --cols 8 --out montage.ppm
+    python examples/shot_montage.py --joint 4          # shots scored on 64-bin joint-colour histograms
 """
 import argparse
 import os
@@ -27,6 +28,8 @@ def main():
     ap.add_argument("--cols", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=16, help="adaptive detector window W")
     ap.add_argument("--out", default="montage.ppm")
+    ap.add_argument("--joint", type=int, default=0,
+                    help="J > 0: score shots on joint-colour histograms (J bins per channel, J^3 bins)")
     a = ap.parse_args()
 
     wl = scn_synth.WORKLOADS["C2"]                       # 1920x1080 synthetic film
@@ -35,10 +38,18 @@ def main():
     job = scn_harness.DeviceJob(wl, 0, M, with_halo=True, plan_=plan)   # frames resident in HBM
 
     # job 1: HIST + shot-diff, then the bounded-state detector (cut if D > 4 x mean of last W + W*H/8)
-    out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
-    scn.scn_run_hist_shotdiff(job.seq, 0, M, wl.bins, out["hist"], out["diff"], out["scratch"])
+    if a.joint:  # NEXT N4's joint-colour variant: J^3 counters per frame, the same [-1,0] stencil
+        J = a.joint
+        hist = torch.empty((M, J ** 3), dtype=torch.int32, device="cuda")
+        diff = torch.empty(M, dtype=torch.int32, device="cuda")
+        scratch = torch.empty(J ** 3, dtype=torch.int32, device="cuda")
+        scn.scn_run_hist_shotdiff_joint(job.seq, 0, M, J, hist, diff, scratch)
+    else:
+        out = job.alloc_outputs(("hist", "shotdiff"), wl.bins)
+        scn.scn_run_hist_shotdiff(job.seq, 0, M, wl.bins, out["hist"], out["diff"], out["scratch"])
+        diff = out["diff"]
     cuts = torch.empty(M, dtype=torch.uint8, device="cuda")
-    scn.scn_run_adaptive_cuts(job.seq, 0, M, a.warmup, out["diff"], 4, 1, wl.width * wl.height // 8, cuts)
+    scn.scn_run_adaptive_cuts(job.seq, 0, M, a.warmup, diff, 4, 1, wl.width * wl.height // 8, cuts)
     starts = [0] + (torch.nonzero(cuts).flatten().cpu().numpy()).tolist()
 
     # job 2: gather the first frame of every shot, downsample into montage tiles
